@@ -1,0 +1,169 @@
+/*
+ * hodlrqr_b200.h -- C ABI of the B200 HODLR-QR kernel library (libhqb200.so).
+ *
+ * The reference (hodlrqr, pure Python/numpy) has no native FFI; its hot path
+ * is the Python call chain
+ *     hqr()                 pkg/src/hodlrqr/hqr.py:80-92
+ *       hqr_rec()           pkg/src/hodlrqr/hqr.py:95-194
+ *         block_qr()        pkg/src/hodlrqr/wy.py:75-88      (leaf compressed column)
+ *         truncate_lowrank  pkg/src/hodlrqr/core.py:239-258  (T_eps recompression)
+ *         apply_dense /     pkg/src/hodlrqr/arith.py:35-64   (HODLR x dense)
+ *         apply_transpose_dense
+ *         low_rank_update   pkg/src/hodlrqr/arith.py:126-145
+ *       hodlr_spectral_norm pkg/src/hodlrqr/arith.py:293-298 (power iteration)
+ * The Python package paper_1809_10585_b200 keeps that API and drives this
+ * library through ctypes.  Every entry point launches ONE batched kernel over
+ * an array of problem descriptors that lives in device memory; dimensions
+ * marked *_ri are read at run time from the device rank table (int32), so a
+ * whole factorization is a fixed launch sequence that can be captured into a
+ * CUDA graph once per tree shape and replayed.
+ *
+ * All matrices are FP64, column-major.  A dimension pair (d, d_ri) means: the
+ * value is rank[d_ri] clamped to d when d_ri >= 0, otherwise d.
+ * Every launcher returns 0 on success or a cudaError_t code.
+ */
+#ifndef HODLRQR_B200_H
+#define HODLRQR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- descriptors (layouts mirrored by numpy dtypes in _abi.py) ---------- */
+
+/* one term alpha * op(A) * op(B); mask: 0 full, 1 upper incl. diagonal,
+   2 unit lower (strict lower + ones); masks act on the STORED matrix */
+typedef struct hq_gemm_term {
+  const double* a;
+  const double* b;
+  int32_t lda, ldb;
+  int32_t ta, tb;
+  int32_t k, k_ri;
+  int32_t mask_a, mask_b;
+  double alpha;
+} hq_gemm_term;
+
+/* C (m x n) = beta*C + sum_t term_t   (reference: every @ in arith.py/hqr.py) */
+typedef struct hq_gemm_prob {
+  double* c;
+  int32_t ldc;
+  int32_t m, m_ri, n, n_ri;
+  int32_t term0, nterm;
+  int32_t pad_;
+  double beta;
+} hq_gemm_prob;
+
+/* a column block of a concatenation [alpha_1 P_1, alpha_2 P_2, ...] */
+typedef struct hq_piece {
+  const double* p;
+  int32_t ld;
+  int32_t cols, cols_ri;
+  int32_t pad_;
+  double alpha;
+} hq_piece;
+
+/* dst (rows x sum cols) = concat(pieces); optional copy into dst2;
+   the total column count is written to rank[ktot_ri]
+   (reference: np.hstack of factors before truncate_lowrank, hqr.py:145,154) */
+typedef struct hq_concat_prob {
+  double* dst;
+  double* dst2;
+  int32_t ldd, ldd2;
+  int32_t rows;
+  int32_t piece0, npiece;
+  int32_t ktot_ri;
+} hq_concat_prob;
+
+/* in-place Householder QR of W (m x k): R on/above the diagonal, unit-lower
+   reflectors below, gamma in tau, per-panel T in tpanel; optional full
+   compact-WY T (k x k) into tfull (reference: wy.py:17-72, dense.py:45-68) */
+typedef struct hq_qr_prob {
+  double* w;
+  double* tau;
+  double* tpanel;
+  double* tfull;
+  int32_t ldw, ldt;
+  int32_t m, m_ri, k, k_ri;
+} hq_qr_prob;
+
+/* X (m x c) := Q X (trans=0) or Q^T X (trans=1) with Q from an hq_qr_prob;
+   when x0 != NULL, X is first set to [x0 (r0 x c); 0] */
+typedef struct hq_applyq_prob {
+  const double* w;
+  const double* tau;
+  const double* tpanel;
+  double* x;
+  const double* x0;
+  int32_t ldw, ldx, ldx0;
+  int32_t m, m_ri, k, k_ri;
+  int32_t c, c_ri;
+  int32_t r0, r0_ri;
+  int32_t trans;
+} hq_applyq_prob;
+
+/* one-sided Jacobi SVD of C (m x n, destroyed).  Keeps the k' columns with
+   sigma > thr, thr = eps_scale * scal[eps_slot] (eps_slot < 0: eps_scale),
+   writes left singular vectors U_k (m x k', sigma descending) and k' into
+   rank[rank_ri]; k' > cap sets rank[flag_ri] = 1 and clamps
+   (reference: svd + truncation_rank in core.py:250-253, dense.py:93-99) */
+typedef struct hq_svd_prob {
+  double* c;
+  double* u;
+  int32_t ldc, ldu;
+  int32_t m, m_ri, n, n_ri;
+  int32_t cap, rank_ri, flag_ri, eps_slot;
+  double eps_scale;
+} hq_svd_prob;
+
+/* a slab of reduced-away rows B_R of an ancestor (hqr.py:112,127) */
+typedef struct hq_slab {
+  const double* v;   /* V factor rows for this leaf: element (i,c) = v[c + i*ld] */
+  double* yv;        /* destination of the matching rows of Y (same layout) */
+  int32_t ld, ldy;
+  int32_t k_ri;
+  int32_t pad_;
+} hq_slab;
+
+/* compressed leaf column [A_leaf; B_R; C] (hqr.py:110-119) */
+typedef struct hq_leaf_prob {
+  double* leaf;
+  double* panel;
+  int32_t nl, ldp;
+  int32_t slab0, nslab;
+  int32_t m_ri;
+  int32_t pad_;
+} hq_leaf_prob;
+
+/* ---- launchers ---------------------------------------------------------- */
+int hq_abi_version(void);
+int hq_device_check(void);
+
+/* grid = tiles x nprob x ksplit; ksplit > 1 accumulates atomically into a
+   pre-zeroed C (beta ignored); skip != NULL && *skip != 0 makes it a no-op */
+int hq_gemm(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
+            int* rank, int tiles, int ksplit, const int* skip);
+int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_piece* pieces,
+              int* rank, int max_rows);
+int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank);
+int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank);
+int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal);
+int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,
+                   int* rank, int max_nl);
+int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,
+                    int* rank, int max_nl);
+/* zero a list of (ptr, count) regions: regions[2i] = ptr, regions[2i+1] = count */
+int hq_zero(void* stream, const int64_t* regions, int nregion, int64_t max_count);
+/* one step of the two-vector power iteration for ||A||_2 (dense.py:102-141),
+   batched: matrix b uses x + 2nb, w + 2nb, g + 4b, scal[2b] (estimate),
+   scal[2b+1] (eps * estimate), done[b]; all_done[0] is set once every matrix
+   has converged (all_done[1] counts) and gates the batched hq_gemm calls */
+int hq_power_step(void* stream, double* x, double* w, const double* g, int n, int ncol,
+                  double* scal, double eps, double tol, int* done, int* all_done, int nmat,
+                  int final_step);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HODLRQR_B200_H */

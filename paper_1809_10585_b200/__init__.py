@@ -1,0 +1,19 @@
+"""B200-native recursive Householder QR of HODLR matrices (arXiv 1809.10585).
+
+Drop-in for the reference package ``hodlrqr``'s hot path: build a HODLR
+matrix with the host containers, then ``hqr(a, eps)`` factors it on the GPU
+(libhqb200.so, sm_100a) into Y, T, R with A ~= (I - Y T Y^T) R.
+"""
+
+from .hodlr import (GENERAL, UNIT_LOWER_TRIANGULAR, UPPER_TRIANGULAR, HodlrMatrix,
+                    LowRankBlock, PartitionTree, TruncationControl, build_partition,
+                    hodlr_identity, stats, to_dense, validate_structure)
+from .hqr import (HodlrQRFactors, HQREngine, PlanIO, RankCapacityError, engine_for, hqr,
+                  hqr_batched)
+
+__version__ = "0.1.0"
+
+__all__ = ["GENERAL", "UNIT_LOWER_TRIANGULAR", "UPPER_TRIANGULAR", "HodlrMatrix", "LowRankBlock",
+           "PartitionTree", "TruncationControl", "build_partition", "hodlr_identity", "stats",
+           "to_dense", "validate_structure", "HodlrQRFactors", "HQREngine", "PlanIO",
+           "RankCapacityError", "engine_for", "hqr", "hqr_batched"]

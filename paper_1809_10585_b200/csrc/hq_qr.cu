@@ -1,0 +1,392 @@
+// Householder QR with compact-WY panels, Q application, and the gathers that
+// build the compressed columns / factor stacks.
+//   QR      reference wy.py:17-72 (+ dense.py:45-68 sign convention)
+//   applyQ  reference wy.py:91-95 / hqr.py:197-216 (Q^T M = M - Y T^T Y^T M)
+//   leaf    reference hqr.py:110-119 (compressed column [A; B_R; C])
+//   concat  reference hqr.py:145,154 / arith.py:107 (stacked low-rank factors)
+// One CTA per problem; panels of NB columns are staged in shared memory when
+// they fit, otherwise reduced in place in (L2-resident) global memory.
+#include "hq_common.cuh"
+
+namespace {
+constexpr int NT = 256, NW = NT / 32, NB = 16;
+constexpr int STAGE_ROWS = 1024;  // panel staged in smem when rows <= STAGE_ROWS
+constexpr int CW = 32;            // trailing-update column chunk
+
+struct QrSmem {
+  double panel[STAGE_ROWS * NB];
+  double tp[NB * NB];
+  double d[NW][NB];
+  double dv[NB];
+  double tcol[NB];
+  double wc[NB * CW];
+  double wc2[NB * CW];
+  double red[32];
+  double scal[4];
+};
+
+// Factor panel P (rows x pw, leading dim ldp; smem or global) into R + unit
+// lower reflectors, gammas into tau[0..pw), and its T factor into S.tp.
+__device__ void panel_factor(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int j = 0; j < pw; ++j) {
+    double ss = 0.0;
+    for (int i = j + 1 + t; i < rows; i += NT) { const double v = P[i + (size_t)j * ldp]; ss += v * v; }
+    ss = block_sum(ss, S.red);
+    if (t == 0) {
+      const double x0 = P[j + (size_t)j * ldp];
+      const double nrm = sqrt(x0 * x0 + ss);
+      double gamma = 0.0, rho = 0.0, inv = 0.0;
+      if (nrm != 0.0) {
+        const double sg = x0 < 0.0 ? -1.0 : 1.0;   // sign(0) := +1
+        const double u1 = x0 + sg * nrm;           // no cancellation
+        rho = -sg * nrm;
+        inv = 1.0 / u1;
+        gamma = 2.0 / (1.0 + ss * inv * inv);
+      }
+      P[j + (size_t)j * ldp] = rho;
+      S.scal[0] = gamma; S.scal[1] = inv;
+      tau[j] = gamma;
+    }
+    __syncthreads();
+    const double gamma = S.scal[0], inv = S.scal[1];
+    for (int i = j + 1 + t; i < rows; i += NT) P[i + (size_t)j * ldp] *= inv;
+    __syncthreads();
+    // d_c = y_j^T P[:, c] for every panel column c != j (rows >= j).  For c < j
+    // these are Y_c^T y_j (T recurrence), for c > j the reflector application.
+    double acc[NB];
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[c] = 0.0;
+    for (int i = j + t; i < rows; i += NT) {
+      const double yi = (i == j) ? 1.0 : P[i + (size_t)j * ldp];
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c < pw && c != j) acc[c] = fma(yi, P[i + (size_t)c * ldp], acc[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      const double v = warp_sum(acc[c]);
+      if (lane == 0) S.d[wid][c] = v;
+    }
+    __syncthreads();
+    if (t < NB) {
+      double v = 0.0;
+      for (int w = 0; w < NW; ++w) v += S.d[w][t];
+      S.dv[t] = v;
+    }
+    __syncthreads();
+    // T[0:j, j] = -gamma * T[0:j, 0:j] d[0:j];  T[j, j] = gamma   (wy.py:37-39)
+    if (t < j) {
+      double v = 0.0;
+      for (int a = t; a < j; ++a) v = fma(S.tp[t + a * NB], S.dv[a], v);
+      S.tcol[t] = -gamma * v;
+    }
+    __syncthreads();
+    if (t < j) S.tp[t + j * NB] = S.tcol[t];
+    if (t == j) S.tp[j + j * NB] = gamma;
+    for (int i = j + t; i < rows; i += NT) {
+      const double yi = (i == j) ? 1.0 : P[i + (size_t)j * ldp];
+      for (int c = j + 1; c < pw; ++c) P[i + (size_t)c * ldp] -= gamma * S.dv[c] * yi;
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ double yval(const double* P, int ldp, int i, int a) {
+  return i == a ? 1.0 : (i > a ? P[i + (size_t)a * ldp] : 0.0);
+}
+
+// W_blk (rows x cw at col) -= Y (T^op (Y^T W_blk)); Y = panel reflectors
+// (rows x pw, local diag at a), tp its T.  trans_t: use T^T (Q^T) else T (Q).
+__device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, const double* tp,
+                                 double* X, int ldx, int ncols, bool trans_t, QrSmem& S) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int c0 = 0; c0 < ncols; c0 += CW) {
+    const int cw = min(CW, ncols - c0);
+    for (int cc = wid; cc < cw; cc += NW) {
+      const double* col = X + (size_t)(c0 + cc) * ldx;
+      double acc[NB];
+#pragma unroll
+      for (int a = 0; a < NB; ++a) acc[a] = 0.0;
+      for (int i = lane; i < rows; i += 32) {
+        const double x = col[i];
+#pragma unroll
+        for (int a = 0; a < NB; ++a)
+          if (a < pw) acc[a] = fma(yval(Y, ldy, i, a), x, acc[a]);
+      }
+#pragma unroll
+      for (int a = 0; a < NB; ++a) {
+        const double v = warp_sum(acc[a]);
+        if (lane == 0) S.wc[a + cc * NB] = v;
+      }
+    }
+    __syncthreads();
+    for (int e = t; e < pw * cw; e += NT) {
+      const int a = e % pw, cc = e / pw;
+      double v = 0.0;
+      if (trans_t) { for (int b = 0; b <= a; ++b) v = fma(tp[b + a * NB], S.wc[b + cc * NB], v); }
+      else { for (int b = a; b < pw; ++b) v = fma(tp[a + b * NB], S.wc[b + cc * NB], v); }
+      S.wc2[a + cc * NB] = v;
+    }
+    __syncthreads();
+    for (int cc = wid; cc < cw; cc += NW) {
+      double* col = X + (size_t)(c0 + cc) * ldx;
+      for (int i = lane; i < rows; i += 32) {
+        double v = col[i];
+        for (int a = 0; a < pw; ++a) v = fma(-yval(Y, ldy, i, a), S.wc2[a + cc * NB], v);
+        col[i] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ probs,
+                                                int* __restrict__ rank) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  QrSmem& S = *reinterpret_cast<QrSmem*>(smem_raw);
+  const hq_qr_prob Q = probs[blockIdx.x];
+  const int m = hq_dim(rank, Q.m, Q.m_ri), k = hq_dim(rank, Q.k, Q.k_ri);
+  const int r = m < k ? m : k;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  double* W = Q.w;
+  const int ld = Q.ldw;
+  for (int p0 = 0; p0 < r; p0 += NB) {
+    const int pw = min(NB, r - p0), rows = m - p0;
+    double* Pg = W + p0 + (size_t)p0 * ld;
+    const bool staged = rows <= STAGE_ROWS;
+    double* P = Pg;
+    int ldp = ld;
+    if (staged) {
+      P = S.panel; ldp = rows;
+      for (int e = t; e < rows * pw; e += NT) P[e % rows + (e / rows) * ldp] = Pg[e % rows + (size_t)(e / rows) * ld];
+    }
+    if (t < NB * NB) S.tp[t] = 0.0;
+    __syncthreads();
+    panel_factor(P, ldp, rows, pw, Q.tau + p0, S);
+    if (Q.tpanel && t < NB * NB) Q.tpanel[(size_t)(p0 / NB) * NB * NB + t] = S.tp[t];
+    // trailing columns: A_trail := Q_p^T A_trail
+    if (p0 + pw < k)
+      apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S);
+    if (staged) {
+      for (int e = t; e < rows * pw; e += NT) Pg[e % rows + (size_t)(e / rows) * ld] = P[e % rows + (e / rows) * ldp];
+    }
+    __syncthreads();
+    // full compact-WY T: T[0:p0, p] = -T[0:p0,0:p0] (Y[:,0:p0]^T Y_p) T_p   (wy.py:53)
+    if (Q.tfull) {
+      double* TF = Q.tfull;
+      const int ldt = Q.ldt;
+      for (int e = t; e < pw * pw; e += NT) TF[(p0 + e % pw) + (size_t)(p0 + e / pw) * ldt] = S.tp[e % pw + (e / pw) * NB];
+      for (int e = t; e < pw * p0; e += NT) TF[(e % p0) + (size_t)(p0 + e / p0) * ldt] = 0.0;
+      __syncthreads();
+      if (p0 > 0) {
+        // X = Y[:,0:p0]^T Y_p, b = row (previous reflector), a = panel reflector
+        for (int b = wid; b < p0; b += NW) {
+          double acc[NB];
+#pragma unroll
+          for (int a = 0; a < NB; ++a) acc[a] = 0.0;
+          for (int i = lane; i < rows; i += 32) {
+            const double yb = W[(p0 + i) + (size_t)b * ld];   // p0+i > b: stored reflector
+#pragma unroll
+            for (int a = 0; a < NB; ++a)
+              if (a < pw) acc[a] = fma(yb, yval(Pg, ld, i, a), acc[a]);
+          }
+#pragma unroll
+          for (int a = 0; a < NB; ++a) {
+            const double v = warp_sum(acc[a]);
+            if (lane == 0) TF[b + (size_t)(p0 + a) * ldt] = v;   // temp: X in place
+          }
+        }
+        __syncthreads();
+        // X := X T_p (p0 x pw), row by row in registers
+        for (int b = t; b < p0; b += NT) {
+          double xr[NB], out[NB];
+          for (int a = 0; a < pw; ++a) xr[a] = TF[b + (size_t)(p0 + a) * ldt];
+          for (int a = 0; a < pw; ++a) {
+            double v = 0.0;
+            for (int c = 0; c <= a; ++c) v = fma(xr[c], S.tp[c + a * NB], v);
+            out[a] = v;
+          }
+          for (int a = 0; a < pw; ++a) TF[b + (size_t)(p0 + a) * ldt] = out[a];
+        }
+        __syncthreads();
+        // T12 = -T11 X  (T11 upper p0 x p0); rows processed top-down in place is
+        // safe since row b only reads rows >= b of X: do bottom-up
+        for (int a = 0; a < pw; ++a) {
+          double* xc = TF + (size_t)(p0 + a) * ldt;
+          // y_b = -sum_{c>=b} T11[b,c] x_c ; compute into registers by thread per b
+          double v[4] = {0, 0, 0, 0};
+          int nb = 0;
+          for (int b = t; b < p0 && nb < 4; b += NT, ++nb) {
+            double s = 0.0;
+            for (int c = b; c < p0; ++c) s = fma(TF[b + (size_t)c * ldt], xc[c], s);
+            v[nb] = -s;
+          }
+          __syncthreads();
+          nb = 0;
+          for (int b = t; b < p0 && nb < 4; b += NT, ++nb) xc[b] = v[nb];
+          __syncthreads();
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// X := Q X (trans = 0) or Q^T X (trans = 1), optionally X := [x0; 0] first.
+__global__ void __launch_bounds__(NT) applyq_kernel(const hq_applyq_prob* __restrict__ probs,
+                                                    int* __restrict__ rank) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  QrSmem& S = *reinterpret_cast<QrSmem*>(smem_raw);
+  const hq_applyq_prob A = probs[blockIdx.x];
+  const int m = hq_dim(rank, A.m, A.m_ri), k = hq_dim(rank, A.k, A.k_ri);
+  const int c = hq_dim(rank, A.c, A.c_ri);
+  const int r = m < k ? m : k;
+  const int t = threadIdx.x;
+  if (m <= 0 || c <= 0) return;
+  if (A.x0) {
+    const int r0 = hq_dim(rank, A.r0, A.r0_ri);
+    for (size_t e = t; e < (size_t)m * c; e += NT) {
+      const int i = (int)(e % m), j = (int)(e / m);
+      A.x[i + (size_t)j * A.ldx] = i < r0 ? A.x0[i + (size_t)j * A.ldx0] : 0.0;
+    }
+    __syncthreads();
+  }
+  const int np = (r + NB - 1) / NB;
+  for (int s = 0; s < np; ++s) {
+    const int p = A.trans ? s : np - 1 - s;
+    const int p0 = p * NB, pw = min(NB, r - p0), rows = m - p0;
+    if (t < NB * NB) S.tp[t] = A.tpanel[(size_t)p * NB * NB + t];
+    __syncthreads();
+    apply_panel_cols(A.w + p0 + (size_t)p0 * A.ldw, A.ldw, rows, pw, S.tp, A.x + p0, A.ldx, c,
+                     A.trans != 0, S);
+  }
+}
+
+// dst (rows x K) = [alpha_1 P_1 | alpha_2 P_2 | ...]; K -> rank[ktot_ri]
+__global__ void concat_kernel(const hq_concat_prob* __restrict__ probs,
+                              const hq_piece* __restrict__ pieces, int* __restrict__ rank) {
+  const hq_concat_prob C = probs[blockIdx.y];
+  int col = 0;
+  for (int q = 0; q < C.npiece; ++q) {
+    const hq_piece Pc = pieces[C.piece0 + q];
+    const int nc = hq_dim(rank, Pc.cols, Pc.cols_ri);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C.rows; i += gridDim.x * blockDim.x) {
+      for (int j = 0; j < nc; ++j) {
+        const double v = Pc.alpha * Pc.p[i + (size_t)j * Pc.ld];
+        C.dst[i + (size_t)(col + j) * C.ldd] = v;
+        if (C.dst2) C.dst2[i + (size_t)(col + j) * C.ldd2] = v;
+      }
+    }
+    col += nc;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && C.ktot_ri >= 0) rank[C.ktot_ri] = col;
+}
+
+// panel = [leaf; slab_1^T; slab_2^T; ...]  (compressed leaf column)
+__global__ void leaf_gather_kernel(const hq_leaf_prob* __restrict__ probs,
+                                   const hq_slab* __restrict__ slabs, int* __restrict__ rank) {
+  const hq_leaf_prob L = probs[blockIdx.y];
+  const int nl = L.nl;
+  const int c = blockIdx.x;  // column
+  if (c >= nl) return;
+  for (int i = threadIdx.x; i < nl; i += blockDim.x)
+    L.panel[i + (size_t)c * L.ldp] = L.leaf[i + (size_t)c * nl];
+  int row = nl;
+  for (int s = 0; s < L.nslab; ++s) {
+    const hq_slab B = slabs[L.slab0 + s];
+    const int kk = rank[B.k_ri];
+    for (int i = threadIdx.x; i < kk; i += blockDim.x)
+      L.panel[row + i + (size_t)c * L.ldp] = B.v[c + (size_t)i * B.ld];
+    row += kk;
+  }
+  if (c == 0 && threadIdx.x == 0 && L.m_ri >= 0) rank[L.m_ri] = row;
+}
+
+// leaf <- panel[0:nl, :] (R + Y), slab Y rows -> yv
+__global__ void leaf_scatter_kernel(const hq_leaf_prob* __restrict__ probs,
+                                    const hq_slab* __restrict__ slabs, int* __restrict__ rank) {
+  const hq_leaf_prob L = probs[blockIdx.y];
+  const int nl = L.nl;
+  const int c = blockIdx.x;
+  if (c >= nl) return;
+  for (int i = threadIdx.x; i < nl; i += blockDim.x)
+    L.leaf[i + (size_t)c * nl] = L.panel[i + (size_t)c * L.ldp];
+  int row = nl;
+  for (int s = 0; s < L.nslab; ++s) {
+    const hq_slab B = slabs[L.slab0 + s];
+    const int kk = rank[B.k_ri];
+    for (int i = threadIdx.x; i < kk; i += blockDim.x)
+      B.yv[c + (size_t)i * B.ldy] = L.panel[row + i + (size_t)c * L.ldp];
+    row += kk;
+  }
+}
+
+__global__ void zero_kernel(const int64_t* __restrict__ regions) {
+  double* p = reinterpret_cast<double*>(regions[2 * blockIdx.y]);
+  const int64_t n = regions[2 * blockIdx.y + 1];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    p[e] = 0.0;
+}
+
+bool g_attr_done = false;
+}  // namespace
+
+static int qr_smem_attr() {
+  if (!g_attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QrSmem));
+    if (e != cudaSuccess) return (int)e;
+    e = cudaFuncSetAttribute(applyq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QrSmem));
+    if (e != cudaSuccess) return (int)e;
+    g_attr_done = true;
+  }
+  return 0;
+}
+
+extern "C" int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank) {
+  if (nprob <= 0) return 0;
+  int e = qr_smem_attr();
+  if (e) return e;
+  qr_kernel<<<nprob, NT, sizeof(QrSmem), (cudaStream_t)stream>>>(probs, rank);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank) {
+  if (nprob <= 0) return 0;
+  int e = qr_smem_attr();
+  if (e) return e;
+  applyq_kernel<<<nprob, NT, sizeof(QrSmem), (cudaStream_t)stream>>>(probs, rank);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_concat(void* stream, const hq_concat_prob* probs, int nprob,
+                         const hq_piece* pieces, int* rank, int max_rows) {
+  if (nprob <= 0) return 0;
+  dim3 grid((max_rows + 255) / 256, nprob);
+  if (grid.x == 0) grid.x = 1;
+  concat_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(probs, pieces, rank);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob,
+                              const hq_slab* slabs, int* rank, int max_nl) {
+  if (nprob <= 0) return 0;
+  leaf_gather_kernel<<<dim3(max_nl, nprob), 128, 0, (cudaStream_t)stream>>>(probs, slabs, rank);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob,
+                               const hq_slab* slabs, int* rank, int max_nl) {
+  if (nprob <= 0) return 0;
+  leaf_scatter_kernel<<<dim3(max_nl, nprob), 128, 0, (cudaStream_t)stream>>>(probs, slabs, rank);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_zero(void* stream, const int64_t* regions, int nregion, int64_t max_count) {
+  if (nregion <= 0) return 0;
+  int gx = (int)((max_count + 255) / 256);
+  if (gx > 1024) gx = 1024;
+  if (gx < 1) gx = 1;
+  zero_kernel<<<dim3(gx, nregion), 256, 0, (cudaStream_t)stream>>>(regions);
+  return hq_err(cudaGetLastError());
+}

@@ -1,0 +1,712 @@
+"""Launch plan for the batched, device-resident hQR (Algorithm 2).
+
+The recursion of the reference (hqr.py:95-194) is unrolled ONCE per tree
+shape into a fixed sequence of batched kernel launches.  Every dimension that
+depends on a truncation rank lives in a device int table ("rank slots") and is
+read by the kernels at run time, so the sequence never synchronizes with the
+host and is captured into a CUDA graph that is replayed for every matrix of
+the same shape.  A launch covers all B matrices of a batch and, where the
+algorithm has independent blocks (HODLR x dense products, the low-rank update
+of a whole subtree), all blocks of a tree level at once.
+
+HBM layout (one persistent region, per matrix b, column-major FP64):
+  leafA[j]  n_j x n_j   input leaf -> R (upper) + Y (strict lower)
+  leafT[j]  n_j x n_j   T leaf
+  per internal node u (children c1, c2; m1 = |c1|, m2 = |c2|, kc = min(m1, m2, kcap)):
+  A12U m1 x kc, A12V m2 x kc   a12 = U V^T; after the node's step it holds R's a12
+  A21U m2 x kc, A21V m1 x kc   a21; after left-orthogonalization U = Y's a21 L-factor
+                               and V = the B_R rows ("slab") fed to the leaves below
+  YV21 m1 x kc                 Y's a21 R-factor (transposed): the Y rows of the slab
+  T12U m1 x kc, T12V m2 x kc   T's coupling block
+  rank slots rA12, rA21, rT12
+The compressed column of a leaf (hqr.py:112) is [A_leaf; slabs of every
+first-child ancestor-or-self, restricted to the leaf's columns]; the slab
+updates of hqr.py:158-159 are applied in place to those V factors.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _abi
+from .hodlr import PartitionTree
+
+NB = 16          # QR panel width (hq_qr.cu)
+GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
+SVD_MAX_N = 4096
+
+R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL = range(5)
+REGION_NAMES = ("persist", "phase", "apply", "trunc", "small")
+
+
+class Buf:
+    """Symbolic device address: region + offset in doubles."""
+    __slots__ = ("reg", "off")
+
+    def __init__(self, reg, off):
+        self.reg, self.off = reg, int(off)
+
+    def __add__(self, k):
+        return Buf(self.reg, self.off + int(k))
+
+
+NULL = None
+
+
+@dataclass
+class Dim:
+    cap: int
+    ri: int = -1
+
+
+class Bump:
+    def __init__(self, reg):
+        self.reg, self.top, self.peak = reg, 0, 0
+
+    def alloc(self, n):
+        n = int(max(n, 1))
+        b = Buf(self.reg, self.top)
+        self.top += (n + 7) // 8 * 8
+        self.peak = max(self.peak, self.top)
+        return b
+
+    def reset(self):
+        self.top = 0
+
+
+class Tree:
+    """Node geometry of a PartitionTree: level l, index j."""
+
+    def __init__(self, tree: PartitionTree):
+        self.L = tree.level
+        self.leaf_sizes = [int(s) for s in tree.leaf_sizes]
+        self.size, self.off = {}, {}
+        offs = np.concatenate([[0], np.cumsum(self.leaf_sizes)])
+        for l in range(self.L + 1):
+            span = 1 << (self.L - l)
+            for j in range(1 << l):
+                a, b = j * span, (j + 1) * span
+                self.off[(l, j)] = int(offs[a])
+                self.size[(l, j)] = int(offs[b] - offs[a])
+        self.n = int(offs[-1])
+
+    def is_leaf(self, v):
+        return v[0] == self.L
+
+    @staticmethod
+    def children(v):
+        return (v[0] + 1, 2 * v[1]), (v[0] + 1, 2 * v[1] + 1)
+
+    @staticmethod
+    def parent(v):
+        return (v[0] - 1, v[1] // 2)
+
+    def internal_nodes(self, v):
+        """Internal nodes of the subtree rooted at v (level order)."""
+        out = []
+        for l in range(v[0], self.L):
+            span = 1 << (l - v[0])
+            out += [(l, j) for j in range(v[1] * span, (v[1] + 1) * span)]
+        return out
+
+    def leaves(self, v):
+        span = 1 << (self.L - v[0])
+        return [(self.L, j) for j in range(v[1] * span, (v[1] + 1) * span)]
+
+    def ancestors(self, v, stop):
+        """Proper ancestors of v up to and including stop (nearest first)."""
+        out, u = [], v
+        while u != stop:
+            u = self.parent(u)
+            out.append(u)
+        return out
+
+    def slab_owners(self, v):
+        """First-child ancestors-or-self w of v (nearest first): their parent's
+        a21 block was the B of w's structured column (hqr.py:127)."""
+        out, w = [], v
+        while w[0] > 0:
+            if w[1] % 2 == 0:
+                out.append(w)
+            w = self.parent(w)
+        return out
+
+
+class Layout:
+    """Persistent per-matrix storage (see module docstring)."""
+
+    def __init__(self, tree: Tree, batch: int, kcap: int, bump: Bump, slots):
+        self.t, self.B, self.kcap = tree, batch, kcap
+        self.kc = {}
+        for u in self._all_internal():
+            c1, c2 = tree.children(u)
+            self.kc[u] = max(1, min(tree.size[c1], tree.size[c2], kcap))
+        self.m = []
+        for b in range(batch):
+            d = {"leafA": {}, "leafT": {}, "A12U": {}, "A12V": {}, "A21U": {}, "A21V": {},
+                 "YV21": {}, "T12U": {}, "T12V": {}, "rA12": {}, "rA21": {}, "rT12": {}}
+            for j, nl in enumerate(tree.leaf_sizes):
+                d["leafA"][(tree.L, j)] = bump.alloc(nl * nl)
+                d["leafT"][(tree.L, j)] = bump.alloc(nl * nl)
+            for u in self._all_internal():
+                c1, c2 = tree.children(u)
+                m1, m2, kc = tree.size[c1], tree.size[c2], self.kc[u]
+                for name, rows in (("A12U", m1), ("A12V", m2), ("A21U", m2), ("A21V", m1),
+                                   ("YV21", m1), ("T12U", m1), ("T12V", m2)):
+                    d[name][u] = bump.alloc(rows * kc)
+                for name in ("rA12", "rA21", "rT12"):
+                    d[name][u] = slots.take()
+            n = tree.n
+            d["X"], d["Y"], d["W"] = bump.alloc(2 * n), bump.alloc(2 * n), bump.alloc(2 * n)
+            self.m.append(d)
+        # power-iteration buffers must be contiguous with stride 2n for the batched kernel
+        self.power_stride = None
+
+    def _all_internal(self):
+        return self.t.internal_nodes((0, 0)) if self.t.L > 0 else []
+
+
+class Slots:
+    def __init__(self):
+        self.n = 0
+
+    def take(self, k=1):
+        s = self.n
+        self.n += k
+        return s
+
+
+class Builder:
+    """Unrolls hqr_rec into batched ops with symbolic addresses."""
+
+    def __init__(self, tree: PartitionTree, batch: int, eps: float, absolute: bool,
+                 kcap: int = 512, max_iter: int = 50, tol: float = 1e-3):
+        self.tree = Tree(tree)
+        self.B = batch
+        self.eps, self.absolute = float(eps), bool(absolute)
+        self.max_iter, self.tol = max_iter, tol
+        self.bumps = [Bump(r) for r in range(5)]
+        self.slots = Slots()
+        self.flag_slot = self.slots.take()
+        self.power_done = self.slots.take(batch)
+        self.all_done = self.slots.take(2)
+        self.lay = Layout(self.tree, batch, kcap, self.bumps[R_PERSIST], self.slots)
+        # power buffers: contiguous [X_b], [W_b] with stride 2n, G with stride 4
+        n = self.tree.n
+        self.PX = self.bumps[R_PERSIST].alloc(2 * n * batch)
+        self.PY = self.bumps[R_PERSIST].alloc(2 * n * batch)
+        self.PW = self.bumps[R_PERSIST].alloc(2 * n * batch)
+        self.PG = self.bumps[R_PERSIST].alloc(4 * batch)
+        self.ops = []
+
+    # ------------------------------------------------------------ primitives
+    def _ph(self, n):
+        return self.bumps[R_PHASE].alloc(n)
+
+    def gemm(self, probs, skip=None, ksplit=1):
+        """probs: list of (c, ldc, Dim m, Dim n, beta, [terms]); term =
+        (a, lda, ta, mask_a, b, ldb, tb, mask_b, Dim k, alpha)."""
+        if not probs:
+            return
+        tiles = max(math.ceil(p[2].cap / GEMM_TILE) * math.ceil(p[3].cap / GEMM_TILE) for p in probs)
+        if tiles <= 0:
+            return
+        self.ops.append(("gemm", probs, dict(tiles=tiles, ksplit=ksplit, skip=skip)))
+
+    def zero(self, regions):
+        if regions:
+            self.ops.append(("zero", regions, {}))
+
+    # ------------------------------------------------------------ HODLR x dense
+    def _fset(self, fs, b):
+        d = self.lay.m[b]
+        if fs == "A":
+            return (("a12", d["A12U"], d["A12V"], d["rA12"]), ("a21", d["A21U"], d["A21V"], d["rA21"])), d["leafA"], 0
+        if fs == "Y":
+            return (("a21", d["A21U"], d["YV21"], d["rA21"]),), d["leafA"], 2
+        if fs == "T":
+            return (("a12", d["T12U"], d["T12V"], d["rT12"]),), d["leafT"], 1
+        if fs == "R":
+            return (("a12", d["A12U"], d["A12V"], d["rA12"]),), d["leafA"], 1
+        raise ValueError(fs)
+
+    def happly(self, v, fs, trans, xs, outs, nc, alpha=1.0, beta=0.0, skip=None):
+        """out_b = alpha * op(F_b|subtree v) X_b + beta * out_b for every matrix b.
+        xs/outs: lists of (Buf, ld); nc: (cap, [ri_b]).  Two launches:
+        phase 1 tmp_blk = V^T X (U^T X), phase 2 per leaf: leaf term + sum of
+        U tmp (V tmp) over the blocks covering the leaf (arith.py:35-64)."""
+        t = self.tree
+        v0 = t.off[v]
+        ncap, nris = nc
+        self.bumps[R_APPLY].reset()
+        p1, p2, zeros, kmax = [], [], [], 0
+        tmp = {}
+        for b in range(self.B):
+            blocks, leafbuf, mask = self._fset(fs, b)
+            X, ldx = xs[b]
+            for u in t.internal_nodes(v) if not t.is_leaf(v) else []:
+                c1, c2 = t.children(u)
+                r1, r2 = t.off[c1] - v0, t.off[c2] - v0
+                m1, m2 = t.size[c1], t.size[c2]
+                kc = self.lay.kc[u]
+                for kind, U, V, R in blocks:
+                    rows0, nrows, cols0, ncols = (r1, m1, r2, m2) if kind == "a12" else (r2, m2, r1, m1)
+                    buf = self.bumps[R_APPLY].alloc(kc * ncap)
+                    tmp[(b, u, kind)] = buf
+                    if trans:   # tmp = U^T X[rows]
+                        term = (U[u], nrows, 1, 0, X + rows0, ldx, 0, 0, Dim(nrows), 1.0)
+                        kmax = max(kmax, nrows)
+                    else:       # tmp = V^T X[cols]
+                        term = (V[u], ncols, 1, 0, X + cols0, ldx, 0, 0, Dim(ncols), 1.0)
+                        kmax = max(kmax, ncols)
+                    p1.append((buf, kc, Dim(kc, R[u]), Dim(ncap, nris[b]), 0.0, [term]))
+                    zeros.append((buf, kc * ncap))
+        ksplit = 1
+        if kmax >= 1024:
+            ksplit = min(32, kmax // 256)
+        if p1:
+            if ksplit > 1:
+                self.zero(zeros)
+            self.gemm(p1, skip=skip, ksplit=ksplit)
+        for b in range(self.B):
+            blocks, leafbuf, mask = self._fset(fs, b)
+            X, ldx = xs[b]
+            O, ldo = outs[b]
+            bd = {kind: (U, V, R) for kind, U, V, R in blocks}
+            for lf in t.leaves(v):
+                o, nl = t.off[lf] - v0, t.size[lf]
+                terms = [(leafbuf[lf], nl, 1 if trans else 0, mask, X + o, ldx, 0, 0, Dim(nl), alpha)]
+                for u in t.ancestors(lf, v) if lf != v else []:
+                    c1, c2 = t.children(u)
+                    in_c1 = t.off[lf] < t.off[c2]
+                    if trans:
+                        kind = "a21" if in_c1 else "a12"
+                        base = t.off[c1] if in_c1 else t.off[c2]
+                    else:
+                        kind = "a12" if in_c1 else "a21"
+                        base = t.off[c1] if in_c1 else t.off[c2]
+                    if kind not in bd:
+                        continue
+                    U, V, R = bd[kind]
+                    F = V if trans else U
+                    ldf = t.size[c1] if in_c1 else t.size[c2]
+                    terms.append((F[u] + (t.off[lf] - base), ldf, 0, 0, tmp[(b, u, kind)],
+                                  self.lay.kc[u], 0, 0, Dim(self.lay.kc[u], R[u]), alpha))
+                p2.append((O + o, ldo, Dim(nl), Dim(ncap, nris[b]), beta, terms))
+        self.gemm(p2, skip=skip)
+
+    # ------------------------------------------------------------ T_eps
+    def trunc(self, probs):
+        """Batched recompression (core.py:239-258) of stacked low-rank sums.
+        prob = dict(m, n, L=[(Buf, ld, Dim, alpha)], R=[...V-form...],
+        eps_slot, eps_scale, U=(Buf, ld), V=(Buf, ld), cap, rank_ri)."""
+        if not probs:
+            return
+        z = self.bumps[R_TRUNC]
+        z.reset()
+        cat, cat_pieces, qr, gm_c, svd, apq, gm_m, gm_v = [], [], [], [], [], [], [], []
+        maxrows = 0
+        for p in probs:
+            m, n, cap = p["m"], p["n"], p["cap"]
+            kcap = sum(d.cap for _, _, d, _ in p["L"])
+            assert kcap == sum(d.cap for _, _, d, _ in p["R"]), "L/R piece capacities differ"
+            k1, k2 = min(m, kcap), min(n, kcap)
+            assert k2 <= SVD_MAX_N, "truncation core too wide"
+            WL, WR, WRc = z.alloc(m * kcap), z.alloc(n * kcap), z.alloc(n * kcap)
+            tauL, tauR = z.alloc(kcap), z.alloc(kcap)
+            npan = max(1, math.ceil(kcap / NB))
+            tpL, tpR = z.alloc(npan * NB * NB), z.alloc(npan * NB * NB)
+            C, Uk, Mm = z.alloc(k1 * k2), z.alloc(k1 * cap), z.alloc(kcap * cap)
+            kL, kR = self.slots.take(), self.slots.take()
+            cat.append((WL, None, m, kL, p["L"]))
+            cat.append((WR, WRc, n, kR, p["R"]))
+            maxrows = max(maxrows, m, n)
+            qr.append((WL, tauL, tpL, None, m, 0, Dim(m), Dim(kcap, kL)))
+            qr.append((WR, tauR, tpR, None, n, 0, Dim(n), Dim(kcap, kR)))
+            # C = R1 R2^T (masks: upper on the stored R factors)
+            gm_c.append((C, k1, Dim(k1, kL), Dim(k2, kR), 0.0,
+                         [(WL, m, 0, 1, WR, n, 1, 1, Dim(kcap, kL), 1.0)]))
+            svd.append((C, Uk, k1, k1, Dim(k1, kL), Dim(k2, kR), cap, p["rank_ri"],
+                        self.flag_slot, p["eps_slot"], p["eps_scale"]))
+            U, ldu = p["U"]
+            V, ldv = p["V"]
+            apq.append((WL, tauL, tpL, U, Uk, m, ldu, k1, Dim(m), Dim(kcap, kL),
+                        Dim(cap, p["rank_ri"]), Dim(k1, kL), 0))
+            # Mm = R1^T U_k ; V = WRc Mm  (right factor = P^T L_out, no 1/sigma)
+            gm_m.append((Mm, kcap, Dim(kcap, kL), Dim(cap, p["rank_ri"]), 0.0,
+                         [(WL, m, 1, 1, Uk, k1, 0, 0, Dim(k1, kL), 1.0)]))
+            gm_v.append((V, ldv, Dim(n), Dim(cap, p["rank_ri"]), 0.0,
+                         [(WRc, n, 0, 0, Mm, kcap, 0, 0, Dim(kcap, kL), 1.0)]))
+        self.ops.append(("concat", cat, dict(max_rows=maxrows)))
+        self.ops.append(("qr", qr, {}))
+        self.gemm(gm_c)
+        self.ops.append(("svd", svd, {}))
+        self.ops.append(("applyq", apq, {}))
+        self.gemm(gm_m)
+        self.gemm(gm_v)
+
+    # ------------------------------------------------------------ algorithm
+    def slabs(self, b, v, sub):
+        """(V-rows, Y-rows, ld, rank slot, kc) of every slab owner of v,
+        restricted to the rows of node `sub` (nearest first)."""
+        d, t = self.lay.m[b], self.tree
+        out = []
+        for w in t.slab_owners(v):
+            pw = t.parent(w)
+            o = t.off[sub] - t.off[w]
+            out.append((d["A21V"][pw] + o, d["YV21"][pw] + o, t.size[w], d["rA21"][pw],
+                        self.lay.kc[pw]))
+        return out
+
+    def power_iteration(self, n):
+        """||A||_2 by the two-vector power method (dense.py:102-141); start
+        vectors are uploaded by the host (input independent)."""
+        skip = self.all_done
+        for it in range(self.max_iter):
+            xs = [(self.PX + 2 * n * b, n) for b in range(self.B)]
+            ys = [(self.PY + 2 * n * b, n) for b in range(self.B)]
+            ws = [(self.PW + 2 * n * b, n) for b in range(self.B)]
+            self.happly((0, 0), "A", False, xs, ys, (2, [-1] * self.B), skip=skip)
+            g = [(self.PG + 4 * b, 2, Dim(2), Dim(2), 0.0,
+                  [(self.PY + 2 * n * b, n, 1, 0, self.PY + 2 * n * b, n, 0, 0, Dim(n), 1.0)])
+                 for b in range(self.B)]
+            self.gemm(g, skip=skip)
+            self.happly((0, 0), "A", True, ys, ws, (2, [-1] * self.B), skip=skip)
+            self.ops.append(("power", None, dict(n=n, final=int(it == self.max_iter - 1))))
+
+    def build(self):
+        t = self.tree
+        if not self.absolute:
+            self.power_iteration(t.n)
+        # left-orthogonalize the a21 blocks of the leftmost spine: the only B
+        # blocks never recompressed by an earlier update (core.py:229-236)
+        if t.L > 0:
+            spine = [(l, 0) for l in range(t.L)]
+            probs = []
+            for b in range(self.B):
+                d = self.lay.m[b]
+                for u in spine:
+                    c1, c2 = t.children(u)
+                    kc = self.lay.kc[u]
+                    probs.append(dict(m=t.size[c2], n=t.size[c1],
+                                      L=[(d["A21U"][u], t.size[c2], Dim(kc, d["rA21"][u]), 1.0)],
+                                      R=[(d["A21V"][u], t.size[c1], Dim(kc, d["rA21"][u]), 1.0)],
+                                      eps_slot=-1, eps_scale=0.0, U=(d["A21U"][u], t.size[c2]),
+                                      V=(d["A21V"][u], t.size[c1]), cap=kc, rank_ri=d["rA21"][u]))
+            self.trunc(probs)
+        self.rec((0, 0))
+        return self
+
+    def eps_slot(self, b):
+        return 2 * b + 1
+
+    def rec(self, v):
+        t = self.tree
+        if t.is_leaf(v):
+            self.leaf_qr(v)
+            return
+        c1, c2 = t.children(v)
+        self.rec(c1)
+        self.s_phase(v)
+        self.rec(c2)
+        self.t_phase(v)
+
+    def leaf_qr(self, v):
+        """Compressed leaf column -> block_qr (hqr.py:110-119)."""
+        t = self.tree
+        self.bumps[R_PHASE].reset()
+        nl = t.size[v]
+        gat, qr = [], []
+        for b in range(self.B):
+            d = self.lay.m[b]
+            sl = self.slabs(b, v, v)
+            mcap = nl + sum(s[4] for s in sl)
+            panel = self._ph(mcap * nl)
+            tau = self._ph(nl)
+            tp = self._ph(math.ceil(nl / NB) * NB * NB)
+            m_ri = self.slots.take()
+            gat.append((d["leafA"][v], panel, nl, mcap, [(s[0], s[1], s[2], s[2], s[3]) for s in sl],
+                        m_ri))
+            qr.append((panel, tau, tp, d["leafT"][v], mcap, nl, Dim(mcap, m_ri), Dim(nl)))
+        self.ops.append(("leaf_gather", gat, dict(max_nl=nl)))
+        self.ops.append(("qr", qr, {}))
+        self.ops.append(("leaf_scatter", gat, dict(max_nl=nl)))
+
+    def s_phase(self, v):
+        """hqr.py:134-159: S~ (one recompression of the four-term sum), S, the
+        R coupling block, and the update of the second block column."""
+        t = self.tree
+        self.bumps[R_PHASE].reset()
+        c1, c2 = t.children(v)
+        m1, m2 = t.size[c1], t.size[c2]
+        kc = self.lay.kc[v]
+        B = range(self.B)
+        D = [self.lay.m[b] for b in B]
+        cap_s = kc
+        tmp1 = [self._ph(m1 * kc) for _ in B]
+        tmp2 = [self._ph(m2 * kc) for _ in B]
+        # t1 = Y(c1)^T A12.L ; t2 = A(c2)^T QB
+        self.happly(c1, "Y", True, [(D[b]["A12U"][v], m1) for b in B], [(tmp1[b], m1) for b in B],
+                    (kc, [D[b]["rA12"][v] for b in B]))
+        self.happly(c2, "A", True, [(D[b]["A21U"][v], m2) for b in B], [(tmp2[b], m2) for b in B],
+                    (kc, [D[b]["rA21"][v] for b in B]))
+        sL = [self._ph(m1 * cap_s) for _ in B]
+        sR = [self._ph(m2 * cap_s) for _ in B]
+        ks = [self.slots.take() for _ in B]
+        probs = []
+        for b in B:
+            d = D[b]
+            Lp = [(tmp1[b], m1, Dim(kc, d["rA12"][v]), 1.0), (d["YV21"][v], m1, Dim(kc, d["rA21"][v]), 1.0)]
+            Rp = [(d["A12V"][v], m2, Dim(kc, d["rA12"][v]), 1.0), (tmp2[b], m2, Dim(kc, d["rA21"][v]), 1.0)]
+            for (vc1, yc1, ld, ri, kw), (vc2, yc2, _, _, _) in zip(self.slabs(b, v, c1), self.slabs(b, v, c2)):
+                Lp.append((yc1, ld, Dim(kw, ri), 1.0))
+                Rp.append((vc2, ld, Dim(kw, ri), 1.0))
+            probs.append(dict(m=m1, n=m2, L=Lp, R=Rp, eps_slot=self.eps_slot(b), eps_scale=1.0,
+                              U=(sL[b], m1), V=(sR[b], m2), cap=cap_s, rank_ri=ks[b]))
+        self.trunc(probs)
+        # S = T1^T S~ (hqr.py:150)
+        sL2 = [self._ph(m1 * cap_s) for _ in B]
+        self.happly(c1, "T", True, [(sL[b], m1) for b in B], [(sL2[b], m1) for b in B], (cap_s, ks))
+        # R's a12 = T([A12.L, -Y11 S.L], [A12.R; S.R]) (hqr.py:153-155)
+        ys = [self._ph(m1 * cap_s) for _ in B]
+        self.happly(c1, "Y", False, [(sL2[b], m1) for b in B], [(ys[b], m1) for b in B], (cap_s, ks))
+        probs = []
+        for b in B:
+            d = D[b]
+            probs.append(dict(m=m1, n=m2,
+                              L=[(d["A12U"][v], m1, Dim(kc, d["rA12"][v]), 1.0), (ys[b], m1, Dim(cap_s, ks[b]), -1.0)],
+                              R=[(d["A12V"][v], m2, Dim(kc, d["rA12"][v]), 1.0), (sR[b], m2, Dim(cap_s, ks[b]), 1.0)],
+                              eps_slot=self.eps_slot(b), eps_scale=1.0, U=(d["A12U"][v], m1),
+                              V=(d["A12V"][v], m2), cap=kc, rank_ri=d["rA12"][v]))
+        self.trunc(probs)
+        # cross = QB (Y_B S.L) (hqr.py:156)
+        w1 = [self._ph(kc * cap_s) for _ in B]
+        cross = [self._ph(m2 * cap_s) for _ in B]
+        ks1 = min(32, m1 // 256) if m1 >= 1024 else 1
+        if ks1 > 1:
+            self.zero([(w1[b], kc * cap_s) for b in B])
+        self.gemm([(w1[b], kc, Dim(kc, D[b]["rA21"][v]), Dim(cap_s, ks[b]), 0.0,
+                    [(D[b]["YV21"][v], m1, 1, 0, sL2[b], m1, 0, 0, Dim(m1), 1.0)]) for b in B],
+                  ksplit=ks1)
+        self.gemm([(cross[b], m2, Dim(m2), Dim(cap_s, ks[b]), 0.0,
+                    [(D[b]["A21U"][v], m2, 0, 0, w1[b], kc, 0, 0, Dim(kc, D[b]["rA21"][v]), 1.0)]) for b in B])
+        # A22 <- A22 - cross S.R: leaves densely, blocks recompressed (arith.py:126-145)
+        leafp = []
+        for b in B:
+            for lf in t.leaves(c2):
+                o, nl = t.off[lf] - t.off[c2], t.size[lf]
+                leafp.append((D[b]["leafA"][lf], nl, Dim(nl), Dim(nl), 1.0,
+                              [(cross[b] + o, m2, 0, 0, sR[b] + o, m2, 1, 0, Dim(cap_s, ks[b]), -1.0)]))
+        self.gemm(leafp)
+        probs = []
+        for b in B:
+            d = D[b]
+            for u in t.internal_nodes(c2) if not t.is_leaf(c2) else []:
+                u1, u2 = t.children(u)
+                k_u = self.lay.kc[u]
+                for kind in ("a12", "a21"):
+                    if kind == "a12":
+                        rs, rn, cs, cn, U, V, R = u1, t.size[u1], u2, t.size[u2], d["A12U"], d["A12V"], d["rA12"]
+                    else:
+                        rs, rn, cs, cn, U, V, R = u2, t.size[u2], u1, t.size[u1], d["A21U"], d["A21V"], d["rA21"]
+                    ro, co = t.off[rs] - t.off[c2], t.off[cs] - t.off[c2]
+                    probs.append(dict(m=rn, n=cn,
+                                      L=[(U[u], rn, Dim(k_u, R[u]), 1.0), (cross[b] + ro, m2, Dim(cap_s, ks[b]), -1.0)],
+                                      R=[(V[u], cn, Dim(k_u, R[u]), 1.0), (sR[b] + co, m2, Dim(cap_s, ks[b]), 1.0)],
+                                      eps_slot=self.eps_slot(b), eps_scale=1.0, U=(U[u], rn), V=(V[u], cn),
+                                      cap=k_u, rank_ri=R[u]))
+        self.trunc(probs)
+        # slab updates B_R2 -= (Y_B1 S.L) S.R, C2 likewise (hqr.py:158-159)
+        zs, g1, g2, zero = [], [], [], []
+        for b in B:
+            for (vc1, yc1, ld, ri, kw), (vc2, yc2, _, _, _) in zip(self.slabs(b, v, c1), self.slabs(b, v, c2)):
+                zb = self._ph(cap_s * kw)
+                zero.append((zb, cap_s * kw))
+                g1.append((zb, cap_s, Dim(cap_s, ks[b]), Dim(kw, ri), 0.0,
+                           [(sL2[b], m1, 1, 0, yc1, ld, 0, 0, Dim(m1), 1.0)]))
+                g2.append((vc2, ld, Dim(m2), Dim(kw, ri), 1.0,
+                           [(sR[b], m2, 0, 0, zb, cap_s, 0, 0, Dim(cap_s, ks[b]), -1.0)]))
+        if g1:
+            if ks1 > 1:
+                self.zero(zero)
+            self.gemm(g1, ksplit=ks1)
+            self.gemm(g2)
+
+    def t_phase(self, v):
+        """hqr.py:169-181: T~12 (one recompression of the three-term sum) and
+        T12 = -T1 T~12 T2."""
+        t = self.tree
+        self.bumps[R_PHASE].reset()
+        c1, c2 = t.children(v)
+        m1, m2 = t.size[c1], t.size[c2]
+        kc = self.lay.kc[v]
+        B = range(self.B)
+        D = [self.lay.m[b] for b in B]
+        tmp3 = [self._ph(m2 * kc) for _ in B]
+        self.happly(c2, "Y", True, [(D[b]["A21U"][v], m2) for b in B], [(tmp3[b], m2) for b in B],
+                    (kc, [D[b]["rA21"][v] for b in B]))
+        tL = [self._ph(m1 * kc) for _ in B]
+        tR = [self._ph(m2 * kc) for _ in B]
+        probs = []
+        for b in B:
+            d = D[b]
+            Lp = [(d["YV21"][v], m1, Dim(kc, d["rA21"][v]), 1.0)]
+            Rp = [(tmp3[b], m2, Dim(kc, d["rA21"][v]), 1.0)]
+            for (vc1, yc1, ld, ri, kw), (vc2, yc2, _, _, _) in zip(self.slabs(b, v, c1), self.slabs(b, v, c2)):
+                Lp.append((yc1, ld, Dim(kw, ri), 1.0))
+                Rp.append((yc2, ld, Dim(kw, ri), 1.0))
+            probs.append(dict(m=m1, n=m2, L=Lp, R=Rp, eps_slot=-1, eps_scale=self.eps,
+                              U=(tL[b], m1), V=(tR[b], m2), cap=kc, rank_ri=d["rT12"][v]))
+        self.trunc(probs)
+        rT = [D[b]["rT12"][v] for b in B]
+        self.happly(c1, "T", False, [(tL[b], m1) for b in B], [(D[b]["T12U"][v], m1) for b in B],
+                    (kc, rT), alpha=-1.0)
+        self.happly(c2, "T", True, [(tR[b], m2) for b in B], [(D[b]["T12V"][v], m2) for b in B],
+                    (kc, rT))
+
+
+# ---------------------------------------------------------------- packing
+
+def _addr(buf, bases, base_ptr):
+    if buf is None:
+        return 0
+    return base_ptr + 8 * (bases[buf.reg] + buf.off)
+
+
+class CompiledPlan:
+    """Ops packed into one device descriptor buffer; run() launches them."""
+
+    def __init__(self, builder: Builder, device):
+        import torch
+        self.b = builder
+        self.device = device
+        sizes = [bp.peak for bp in builder.bumps]
+        self.region_sizes = sizes
+        bases, acc = [], 0
+        for s in sizes:
+            bases.append(acc)
+            acc += (s + 63) // 64 * 64
+        self.total_doubles = acc
+        self.arena = torch.zeros(max(acc, 1), dtype=torch.float64, device=device)
+        self.rank = torch.zeros(max(builder.slots.n, 1), dtype=torch.int32, device=device)
+        self.scal = torch.zeros(max(2 * builder.B, 2), dtype=torch.float64, device=device)
+        base_ptr = self.arena.data_ptr()
+        self.bases = bases
+        A = lambda buf: _addr(buf, bases, base_ptr)
+        chunks, self.launch = [], []
+        off = 0
+
+        def put(arr):
+            nonlocal off
+            raw = arr.tobytes()
+            start = off
+            chunks.append((start, raw))
+            off = (off + len(raw) + 255) // 256 * 256
+            return start
+
+        for kind, probs, extra in builder.ops:
+            if kind == "gemm":
+                pa = np.zeros(len(probs), _abi.GEMM_PROB)
+                nterm = sum(len(p[5]) for p in probs)
+                ta = np.zeros(nterm, _abi.GEMM_TERM)
+                ti = 0
+                for i, (c, ldc, m, n, beta, terms) in enumerate(probs):
+                    pa[i] = (A(c), ldc, m.cap, m.ri, n.cap, n.ri, ti, len(terms), 0, beta)
+                    for (a, lda, tra, ma, bb, ldb, trb, mb, k, alpha) in terms:
+                        ta[ti] = (A(a), A(bb), lda, ldb, tra, trb, k.cap, k.ri, ma, mb, alpha)
+                        ti += 1
+                self.launch.append(("gemm", put(pa), put(ta), len(probs), extra))
+            elif kind == "zero":
+                ra = np.zeros(2 * len(probs), np.int64)
+                mx = 0
+                for i, (buf, cnt) in enumerate(probs):
+                    ra[2 * i], ra[2 * i + 1] = A(buf), cnt
+                    mx = max(mx, cnt)
+                self.launch.append(("zero", put(ra), None, len(probs), dict(max_count=mx)))
+            elif kind == "concat":
+                pa = np.zeros(len(probs), _abi.CONCAT_PROB)
+                npc = sum(len(p[4]) for p in probs)
+                pc = np.zeros(max(npc, 1), _abi.PIECE)
+                pi = 0
+                for i, (dst, dst2, rows, kri, pieces) in enumerate(probs):
+                    pa[i] = (A(dst), A(dst2), rows, rows, rows, pi, len(pieces), kri)
+                    for (p, ld, d, alpha) in pieces:
+                        pc[pi] = (A(p), ld, d.cap, d.ri, 0, alpha)
+                        pi += 1
+                self.launch.append(("concat", put(pa), put(pc), len(probs), extra))
+            elif kind == "qr":
+                pa = np.zeros(len(probs), _abi.QR_PROB)
+                for i, (w, tau, tp, tf, ldw, ldt, m, k) in enumerate(probs):
+                    pa[i] = (A(w), A(tau), A(tp), A(tf), ldw, ldt, m.cap, m.ri, k.cap, k.ri)
+                self.launch.append(("qr", put(pa), None, len(probs), extra))
+            elif kind == "svd":
+                pa = np.zeros(len(probs), _abi.SVD_PROB)
+                for i, (c, u, ldc, ldu, m, n, cap, rri, fri, es, esc) in enumerate(probs):
+                    pa[i] = (A(c), A(u), ldc, ldu, m.cap, m.ri, n.cap, n.ri, cap, rri, fri, es, esc)
+                self.launch.append(("svd", put(pa), None, len(probs), extra))
+            elif kind == "applyq":
+                pa = np.zeros(len(probs), _abi.APPLYQ_PROB)
+                for i, (w, tau, tp, x, x0, ldw, ldx, ldx0, m, k, c, r0, tr) in enumerate(probs):
+                    pa[i] = (A(w), A(tau), A(tp), A(x), A(x0), ldw, ldx, ldx0, m.cap, m.ri,
+                             k.cap, k.ri, c.cap, c.ri, r0.cap, r0.ri, tr)
+                self.launch.append(("applyq", put(pa), None, len(probs), extra))
+            elif kind in ("leaf_gather", "leaf_scatter"):
+                pa = np.zeros(len(probs), _abi.LEAF_PROB)
+                ns = sum(len(p[4]) for p in probs)
+                sa = np.zeros(max(ns, 1), _abi.SLAB)
+                si = 0
+                for i, (leaf, panel, nl, ldp, slabs, mri) in enumerate(probs):
+                    pa[i] = (A(leaf), A(panel), nl, ldp, si, len(slabs), mri, 0)
+                    for (vv, yv, ld, ldy, kri) in slabs:
+                        sa[si] = (A(vv), A(yv), ld, ldy, kri, 0)
+                        si += 1
+                self.launch.append((kind, put(pa), put(sa), len(probs), extra))
+            elif kind == "power":
+                self.launch.append(("power", None, None, builder.B, extra))
+            else:
+                raise ValueError(kind)
+        blob = bytearray(max(off, 256))
+        for start, raw in chunks:
+            blob[start:start + len(raw)] = raw
+        self.desc = torch.frombuffer(blob, dtype=torch.uint8).clone().to(device)
+        self.n_launch = len(self.launch)
+        self.graph = None
+
+    def addr(self, buf):
+        return _addr(buf, self.bases, self.arena.data_ptr())
+
+    def run(self, stream_handle: int):
+        lib = _abi.load()
+        dp = self.desc.data_ptr()
+        rk = self.rank.data_ptr()
+        sc = self.scal.data_ptr()
+        b = self.b
+        for kind, o1, o2, cnt, ex in self.launch:
+            if kind == "gemm":
+                skip = rk + 4 * ex["skip"] if ex["skip"] is not None else None
+                rc = lib.hq_gemm(stream_handle, dp + o1, cnt, dp + o2, rk, ex["tiles"], ex["ksplit"], skip)
+            elif kind == "zero":
+                rc = lib.hq_zero(stream_handle, dp + o1, cnt, ex["max_count"])
+            elif kind == "concat":
+                rc = lib.hq_concat(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_rows"])
+            elif kind == "qr":
+                rc = lib.hq_qr(stream_handle, dp + o1, cnt, rk)
+            elif kind == "svd":
+                rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc)
+            elif kind == "applyq":
+                rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk)
+            elif kind == "leaf_gather":
+                rc = lib.hq_leaf_gather(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
+            elif kind == "leaf_scatter":
+                rc = lib.hq_leaf_scatter(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
+            elif kind == "power":
+                rc = lib.hq_power_step(stream_handle, self.addr(b.PX), self.addr(b.PW), self.addr(b.PG),
+                                       b.tree.n, 2 if b.tree.n >= 2 else 1, sc, b.eps, b.tol,
+                                       rk + 4 * b.power_done, rk + 4 * b.all_done, b.B, ex["final"])
+            _abi.check(rc, kind)
+
+    def count_kernels(self):
+        return len(self.launch)
