@@ -1,0 +1,301 @@
+#!/usr/bin/env python
+"""Benchmark: HODLR QR factorizations/s (FP64) on the B200.
+
+Workload (BASELINE.json metric "at n=16384"): config 2, the ill-conditioned
+HODLR matrix, n = 16384, leaf 256, off-diagonal rank 16, A = D B with
+D = diag(logspace(0,-14,n)) permuted, tol 1e-10 relative.  One step = one
+full hQR factorization (power iteration for ||A||_2, the unrolled Algorithm 2,
+compaction of Y, T, R) of one matrix.
+
+  value  factorizations/s with the input resident in HBM (graph replay of the
+         whole factorization; CUDA events on the launching stream, max over
+         ranks); the working set (~GBs of factor storage) exceeds the 126 MB L2.
+  e2e    the same metric through the public API with host buffers: pack,
+         H2D of the compact input stream, replay, D2H of the compact factors,
+         and assembly of the HodlrMatrix factors -- all inside the timed region.
+Under torchrun each rank factors its own matrix (seed = rank): independent
+HODLR matrices shard with no collective (weak scaling).
+
+--impl reference times the CPU oracle port (oracle/hqr_oracle.py, a numpy
+restatement of the reference hodlrqr.hqr pinned to its golden vectors) on the
+host cores, on the same configuration.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "hodlr_qr_factorizations_per_s"
+UNIT = "factorizations/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", type=int, default=2)
+    p.add_argument("--n", type=int, default=None, help="override n (smoke runs)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-instrument", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def config_dict(cfg, n, extra=None):
+    from paper_1809_10585_b200.gen import CONFIGS
+    c = dict(CONFIGS[cfg])
+    d = {"workload": f"config{cfg}:{c['name']}", "n": n if n else c["n"], "leaf": c["leaf"],
+         "tol": c["tol"], "offdiag_rank": c.get("rank"), "matrices_per_step_per_gpu": 1,
+         "l2": "working set > 126 MB L2 (factor storage in HBM); no flush needed"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.samples, self.proc = index, [], None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if len(s) >= 6 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 6 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples if len(s) >= 6
+                          for i in range(4) if "Active" in s[2 + i] and "Not" not in s[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def cpu_reference_time(cfg, n, seed=0):
+    """One oracle (numpy CPU) factorization of the workload; seconds."""
+    from oracle import hqr_oracle as O
+    from paper_1809_10585_b200.gen import CONFIGS, gen_config
+    a = gen_config(cfg, seed=seed, n=n)
+    t0 = time.perf_counter()
+    O.hqr(a, CONFIGS[cfg]["tol"])
+    return time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max((i.get("num_threads", 1) for i in info if i.get("user_api") == "blas"), default=1)
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1809_10585_b200.gen import CONFIGS
+    n = args.n or CONFIGS[args.config]["n"]
+    steps = max(1, min(args.steps, 3))
+    warm = 1 if args.warmup > 0 else 0
+    for _ in range(warm):
+        cpu_reference_time(args.config, n)
+    times = [cpu_reference_time(args.config, n, seed=s) for s in range(steps)]
+    t = float(np.mean(times))
+    v = 1.0 / t
+    cores = cpu_cores()
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+            "warmup": warm, "ms_per_step": 1e3 * t, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator of BASELINE config)",
+            "config": config_dict(args.config, n), "impl": "reference",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{steps} full factorization(s) of the workload matrix "
+                                       "(oracle/hqr_oracle.py, numpy + OpenBLAS)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": f"steps capped at {steps} (each step is a full CPU factorization)"}
+    print(json.dumps(line), flush=True)
+
+
+def instrument(eng, torch):
+    """One non-graph pass with CUDA events around every launch: per-kind
+    device time (for the roofline of the dominant kernel)."""
+    plan = eng.plan
+    lib = __import__("paper_1809_10585_b200._abi", fromlist=["load"]).load()
+    s = eng.stream
+    per = {}
+    eng.upload()
+    s.synchronize()
+    evs = []
+    orig = plan.launch
+    with torch.cuda.stream(s):
+        for i, rec in enumerate(orig):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            plan.launch = [rec]
+            plan.run(s.cuda_stream)
+            e1.record(s)
+            evs.append((rec[0], e0, e1))
+    plan.launch = orig
+    s.synchronize()
+    for kind, e0, e1 in evs:
+        d = per.setdefault(kind, [0.0, 0])
+        d[0] += e0.elapsed_time(e1)
+        d[1] += 1
+    del lib
+    return per
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1809_10585_b200.gen import CONFIGS, gen_config
+    from paper_1809_10585_b200.hqr import HQREngine
+    from paper_1809_10585_b200.plan import plan_accounting
+    cfg = CONFIGS[args.config]
+    n = args.n or cfg["n"]
+    a = gen_config(args.config, seed=rank, n=n)
+    eng = HQREngine(a.tree(), 1, cfg["tol"], device=f"cuda:{local}")
+    eng.pack([a])
+    eng.upload()
+    eng.snapshot_device_input()
+    eng.execute()  # capture + first run
+    eng.download()
+    s = eng.stream
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        eng.restore_device_input()
+        eng.execute()
+    s.synchronize()
+    # ---- device-timed region: input resident in HBM
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(s)
+    for _ in range(args.steps):
+        eng.restore_device_input()
+        eng.execute()
+    ev1.record(s)
+    ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ws * args.steps / (ms / 1e3)
+    # ---- end-to-end through the public API with host buffers
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        f = eng.factorize([a])
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if ws > 1:
+        t = torch.tensor([e2e_s], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(eng.h2d_bytes()),
+           "d2h_bytes_per_step": int(eng.d2h_bytes()),
+           "includes": "pack + H2D + graph replay + D2H + HodlrMatrix assembly"}
+    rk = eng.h_rk_out.numpy()
+    acc = plan_accounting(eng.builder, rk)
+    flops = sum(v["flops"] for v in acc.values())
+    from paper_1809_10585_b200.hodlr import stats
+    ranks = {k: stats(getattr(f[0], k))["max_offdiag_rank"] for k in ("y", "t", "r")}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator of BASELINE config; seed = rank)",
+            "config": config_dict(args.config, n, {"parallelism": f"independent matrices x{ws}"}),
+            "e2e": e2e, "gpu_launches": eng.plan.n_launch * args.steps,
+            "fp64_gflops_effective": flops / (ms_step / 1e3) / 1e9,
+            "algorithmic_gflop_per_step": flops / 1e9,
+            "norm_estimate": eng.norm_estimate(0), "max_ranks": ranks, "clocks": clk}
+    if not args.no_instrument and rank == 0:
+        per = instrument(eng, torch)
+        tot = sum(v[0] for v in per.values())
+        kinds = {k: {"ms": v[0], "launches": v[1], "share": v[0] / tot} for k, v in per.items()}
+        top = max((k for k in per if acc.get(k, {}).get("flops", 0) > 0), key=lambda k: per[k][0])
+        peak_fp64 = 37.16e12  # self-measured DMMA m8n8k4 FP64 (profiles/r01_fp64_peak.txt)
+        ach = acc[top]["flops"] / (per[top][0] / 1e3)
+        line["roofline"] = {"kernel": top, "bound": "tensor", "achieved": ach / 1e12, "peak": peak_fp64 / 1e12,
+                            "unit": "TFLOP/s", "frac": ach / peak_fp64, "traffic": None,
+                            "peak_source": "self-measured FP64 DMMA peak (profiles/r01_fp64_peak.txt); "
+                                           "MEASURED_PEAKS.json has no FP64 entry",
+                            "flops_per_launch": acc[top]["flops"] / max(acc[top]["launches"], 1),
+                            "avg_launch_ms": per[top][0] / per[top][1], "share_of_step": kinds[top]["share"]}
+        line["kernel_time_by_kind"] = kinds
+    if rank == 0 and not args.no_cpu_baseline and ws == 1:
+        t_cpu = cpu_reference_time(args.config, n)
+        line["cpu_baseline"] = {"value": 1.0 / t_cpu, "unit": UNIT, "cores": cpu_cores(), "kind": "port",
+                                "sample": "1 full factorization of the workload matrix (oracle/hqr_oracle.py)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -136,6 +136,16 @@ typedef struct hq_leaf_prob {
   int32_t pad_;
 } hq_leaf_prob;
 
+/* one column-major 2D copy dst(rows x cols) = src; cols from the rank table
+   when cols_ri >= 0 (used to restore inputs and to compact the factors for
+   the single device->host copy) */
+typedef struct hq_copy_item {
+  const double* src;
+  double* dst;
+  int32_t rows, cols, cols_ri, lds, ldd;
+  int32_t pad_;
+} hq_copy_item;
+
 /* ---- launchers ---------------------------------------------------------- */
 int hq_abi_version(void);
 int hq_device_check(void);
@@ -153,6 +163,13 @@ int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob, const hq_
                    int* rank, int max_nl);
 int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,
                     int* rank, int max_nl);
+/* copy items (one CTA per item); hq_pack_offsets first rewrites each dst
+   (which = 0) or src (which = 1) as base + exclusive prefix sum of rows*cols
+   (dense packing with run-time ranks) and stores the total (doubles) in
+   total[0] */
+int hq_copy(void* stream, const hq_copy_item* items, int nitem, const int* rank);
+int hq_pack_offsets(void* stream, hq_copy_item* items, int nitem, const int* rank, double* base,
+                    int64_t* total, int which);
 /* zero a list of (ptr, count) regions: regions[2i] = ptr, regions[2i+1] = count */
 int hq_zero(void* stream, const int64_t* regions, int nregion, int64_t max_count);
 /* one step of the two-vector power iteration for ||A||_2 (dense.py:102-141),

@@ -329,6 +329,56 @@ __global__ void zero_kernel(const int64_t* __restrict__ regions) {
     p[e] = 0.0;
 }
 
+__global__ void copy_kernel(const hq_copy_item* __restrict__ items, const int* __restrict__ rank) {
+  const hq_copy_item it = items[blockIdx.x];
+  const int cols = hq_dim(rank, it.cols, it.cols_ri);
+  const size_t n = (size_t)it.rows * cols;
+  for (size_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const int i = (int)(e % it.rows), j = (int)(e / it.rows);
+    it.dst[i + (size_t)j * it.ldd] = it.src[i + (size_t)j * it.lds];
+  }
+}
+
+// single-CTA exclusive scan of rows*cols -> dst = base + offset, ldd = rows
+__global__ void pack_offsets_kernel(hq_copy_item* items, int nitem, const int* rank, double* base,
+                                    int64_t* total, int which) {
+  __shared__ int64_t carry;
+  __shared__ int64_t wsum[32];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < nitem; c0 += blockDim.x) {
+    const int i = c0 + threadIdx.x;
+    int64_t v = 0;
+    if (i < nitem) v = (int64_t)items[i].rows * hq_dim(rank, items[i].cols, items[i].cols_ri);
+    int64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      int64_t w = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    const int64_t excl = carry + x - v + (wid > 0 ? wsum[wid - 1] : 0);
+    if (i < nitem) {
+      if (which) { items[i].src = base + excl; items[i].lds = items[i].rows; }
+      else { items[i].dst = base + excl; items[i].ldd = items[i].rows; }
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) total[0] = carry;
+}
+
 bool g_attr_done = false;
 }  // namespace
 
@@ -388,5 +438,18 @@ extern "C" int hq_zero(void* stream, const int64_t* regions, int nregion, int64_
   if (gx > 1024) gx = 1024;
   if (gx < 1) gx = 1;
   zero_kernel<<<dim3(gx, nregion), 256, 0, (cudaStream_t)stream>>>(regions);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_copy(void* stream, const hq_copy_item* items, int nitem, const int* rank) {
+  if (nitem <= 0) return 0;
+  copy_kernel<<<nitem, 256, 0, (cudaStream_t)stream>>>(items, rank);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_pack_offsets(void* stream, hq_copy_item* items, int nitem, const int* rank,
+                               double* base, int64_t* total, int which) {
+  if (nitem <= 0) return 0;
+  pack_offsets_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(items, nitem, rank, base, total, which);
   return hq_err(cudaGetLastError());
 }

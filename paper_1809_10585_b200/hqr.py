@@ -20,7 +20,7 @@ import numpy as np
 from . import _abi
 from .hodlr import (GENERAL, UNIT_LOWER_TRIANGULAR, UPPER_TRIANGULAR, HodlrMatrix, LowRankBlock,
                     PartitionTree)
-from .plan import R_PERSIST, Builder, CompiledPlan
+from .plan import R_IN, R_OUT, R_PERSIST, Builder, CompiledPlan
 
 
 class RankCapacityError(RuntimeError):
@@ -51,86 +51,91 @@ def _start_vectors(n):
 
 
 class PlanIO:
-    """Host side of a plan: packs inputs into the persistent-region image and
-    assembles HodlrMatrix factors from a downloaded image (no CUDA needed)."""
+    """Host side of a plan: packs inputs into the compact input stream and
+    assembles HodlrMatrix factors from the compact output stream (no CUDA)."""
 
     def __init__(self, tree: PartitionTree, batch: int = 1, eps: float = 1e-10,
                  absolute: bool = False, kcap: int = 512):
         self.tree, self.B, self.eps, self.absolute, self.kcap = tree, batch, eps, absolute, kcap
         self.builder = Builder(tree, batch, eps, absolute, kcap).build()
-        self.n_persist = self.builder.bumps[R_PERSIST].peak
-        self.img = np.zeros(self.n_persist)
-        self.rk = np.zeros(max(self.builder.slots.n, 1), np.int32)
+        bld = self.builder
+        self.inbuf = np.zeros(max(bld.bumps[R_IN].peak, 1))
+        self.outbuf = np.zeros(max(bld.bumps[R_OUT].peak, 1))
+        self.px = np.zeros(2 * bld.tree.n * batch)
+        self.rk = np.zeros(max(bld.slots.n, 1), np.int32)
         self.sc = np.zeros(max(2 * batch, 2))
+        self.n_in = 0
 
-    # ---------------------------------------------------------------- host image
+    @staticmethod
+    def _nodes(a: HodlrMatrix, t):
+        """(level, index) -> HodlrMatrix node."""
+        out = {}
+
+        def walk(h, v):
+            out[v] = h
+            if not h.is_leaf:
+                c1, c2 = t.children(v)
+                walk(h.a11, c1)
+                walk(h.a22, c2)
+        walk(a, (0, 0))
+        return out
+
     def pack(self, mats):
-        """Write the input matrices into the pinned host image."""
+        """Input ranks -> rank table, factors -> compact input stream."""
         if len(mats) != self.B:
             raise ValueError(f"expected {self.B} matrices, got {len(mats)}")
-        img, rk = self.img, self.rk
-        img[:] = 0.0
+        bld = self.builder
+        t, lay = bld.tree, bld.lay
+        rk = self.rk
         rk[:] = 0
-        t = self.builder.tree
-        lay = self.builder.lay
-        leaves = t.leaves((0, 0))
+        chunks = []
         for b, a in enumerate(mats):
             if tuple(a.leaf_sizes()) != tuple(self.tree.leaf_sizes):
                 raise ValueError("matrix does not match the plan's partition tree")
+            nodes = self._nodes(a, t)
             d = lay.m[b]
-
-            def put(buf, arr):
-                flat = np.asarray(arr, dtype=np.float64).ravel(order="F")
-                img[buf.off:buf.off + flat.size] = flat
-
-            def walk(h, v):
-                if h.is_leaf:
-                    put(d["leafA"][v], h.dense)
-                    return
-                c1, c2 = t.children(v)
-                kc = lay.kc[v]
-                for blk, U, V, R in ((h.a12, "A12U", "A12V", "rA12"), (h.a21, "A21U", "A21V", "rA21")):
+            for lf in t.leaves((0, 0)):
+                chunks.append(nodes[lf].dense.ravel(order="F"))
+            for u in (t.internal_nodes((0, 0)) if t.L > 0 else []):
+                h = nodes[u]
+                kc = lay.kc[u]
+                for blk, slot in ((h.a12, "rA12"), (h.a21, "rA21")):
                     if blk.rank > kc:
                         raise RankCapacityError(f"input block rank {blk.rank} exceeds capacity {kc}")
-                    rows = blk.n_rows
-                    cols = blk.n_cols
-                    buf = d[U][v]
-                    img[buf.off:buf.off + rows * blk.rank] = np.asarray(blk.L).ravel(order="F")
-                    buf = d[V][v]
-                    img[buf.off:buf.off + cols * blk.rank] = np.asarray(blk.R.T).ravel(order="F")
-                    rk[d[R][v]] = blk.rank
-                walk(h.a11, c1)
-                walk(h.a22, c2)
-
-            walk(a, (0, 0))
+                    rk[d[slot][u]] = blk.rank
+                chunks += [h.a12.L.ravel(order="F"), h.a12.R.T.ravel(order="F"),
+                           h.a21.L.ravel(order="F"), h.a21.R.T.ravel(order="F")]
             n = t.n
             x0 = _start_vectors(n) if n >= 2 else np.ones((1, 2))
-            off = self.builder.PX.off + 2 * n * b
-            img[off:off + 2 * n] = x0.ravel(order="F")
+            self.px[2 * n * b:2 * n * (b + 1)] = x0.ravel(order="F")
+        flat = np.concatenate(chunks) if chunks else np.zeros(0)
+        self.inbuf[:flat.size] = flat
+        self.n_in = flat.size
         sc = self.sc
         sc[:] = 0.0
         if self.absolute:
             sc[1::2] = self.eps
             for b in range(self.B):
-                rk[self.builder.power_done + b] = 1
-            rk[self.builder.all_done] = 1
-        del leaves
+                rk[bld.power_done + b] = 1
+            rk[bld.all_done] = 1
 
-    def factors(self, b: int, img=None, rk=None) -> HodlrQRFactors:
-        """Assemble the host HodlrMatrix factors of matrix b from an image."""
-        t = self.builder.tree
-        lay = self.builder.lay
-        d = lay.m[b]
-
-        def get(buf, rows, cols):
-            return img[buf.off:buf.off + rows * cols].reshape((rows, cols), order="F").copy()
+    def factors(self, b: int, out=None, rk=None) -> HodlrQRFactors:
+        """Assemble the HodlrMatrix factors of matrix b from the compact output."""
+        bld = self.builder
+        t = bld.tree
+        d = bld.lay.m[b]
+        blocks, off = {}, 0
+        for (buf, rows, cols) in bld.out_items:
+            c = cols.cap if cols.ri < 0 else int(min(max(rk[cols.ri], 0), cols.cap))
+            blocks[(buf.reg, buf.off)] = out[off:off + rows * c].reshape((rows, c), order="F")
+            off += rows * c
+        get = lambda buf: blocks[(buf.reg, buf.off)].copy()
 
         def build(v, which):
             if t.is_leaf(v):
-                nl = t.size[v]
                 if which == "t":
-                    return HodlrMatrix(dense=np.triu(get(d["leafT"][v], nl, nl)), shape_tag=UPPER_TRIANGULAR)
-                full = get(d["leafA"][v], nl, nl)
+                    return HodlrMatrix(dense=np.triu(get(d["leafT"][v])), shape_tag=UPPER_TRIANGULAR)
+                full = get(d["leafA"][v])
                 if which == "r":
                     return HodlrMatrix(dense=np.triu(full), shape_tag=UPPER_TRIANGULAR)
                 y = np.tril(full, -1)
@@ -141,18 +146,16 @@ class PlanIO:
             h1, h2 = build(c1, which), build(c2, which)
             zero12, zero21 = LowRankBlock.zero(m1, m2), LowRankBlock.zero(m2, m1)
             if which == "y":
-                k = int(rk[d["rA21"][v]])
-                a21 = LowRankBlock(get(d["A21U"][v], m2, k), get(d["YV21"][v], m1, k).T, True)
+                a21 = LowRankBlock(get(d["A21U"][v]), get(d["YV21"][v]).T, True)
                 return HodlrMatrix(a11=h1, a22=h2, a12=zero12, a21=a21, shape_tag=UNIT_LOWER_TRIANGULAR)
             if which == "t":
-                k = int(rk[d["rT12"][v]])
-                a12 = LowRankBlock(get(d["T12U"][v], m1, k), get(d["T12V"][v], m2, k).T)
+                a12 = LowRankBlock(get(d["T12U"][v]), get(d["T12V"][v]).T)
             else:
-                k = int(rk[d["rA12"][v]])
-                a12 = LowRankBlock(get(d["A12U"][v], m1, k), get(d["A12V"][v], m2, k).T, True)
+                a12 = LowRankBlock(get(d["A12U"][v]), get(d["A12V"][v]).T, True)
             return HodlrMatrix(a11=h1, a22=h2, a12=a12, a21=zero21, shape_tag=UPPER_TRIANGULAR)
 
         return HodlrQRFactors(y=build((0, 0), "y"), t=build((0, 0), "t"), r=build((0, 0), "r"))
+
 
 class HQREngine(PlanIO):
     """PlanIO + device arena + CUDA graph for batched hQR of same-shape matrices."""
@@ -165,24 +168,59 @@ class HQREngine(PlanIO):
         self.device = torch.device(device if device is not None else "cuda")
         self.plan = CompiledPlan(self.builder, self.device)
         pin = lambda a: torch.from_numpy(a).pin_memory()
-        self.host_img, self.host_rank, self.host_scal = pin(self.img), pin(self.rk), pin(self.sc)
-        self.img, self.rk, self.sc = self.host_img.numpy(), self.host_rank.numpy(), self.host_scal.numpy()
-        self.out_img = torch.zeros(self.n_persist, dtype=torch.float64).pin_memory()
-        self.out_rank = torch.zeros(self.plan.rank.numel(), dtype=torch.int32).pin_memory()
+        self.h_in, self.h_rk, self.h_sc, self.h_px = pin(self.inbuf), pin(self.rk), pin(self.sc), pin(self.px)
+        self.inbuf, self.rk, self.sc, self.px = (self.h_in.numpy(), self.h_rk.numpy(), self.h_sc.numpy(),
+                                                 self.h_px.numpy())
+        self.h_out = pin(self.outbuf)
+        self.outbuf = self.h_out.numpy()
+        self.h_rk_out = torch.zeros_like(self.h_rk).pin_memory()
+        self.h_tot = torch.zeros(2, dtype=torch.int64).pin_memory()
+        p = self.plan
+        ib, ob = p.bases[R_IN], p.bases[R_OUT]
+        self.d_in = p.arena[ib:ib + self.inbuf.size]
+        self.d_out = p.arena[ob:ob + self.outbuf.size]
+        pxo = p.bases[R_PERSIST] + self.builder.PX.off
+        self.d_px = p.arena[pxo:pxo + self.px.size]
+        self.n_out = 0
         self.use_graph = use_graph
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.device)
 
-    # ---------------------------------------------------------------- device
-    def _launch(self):
-        self.plan.run(self.stream.cuda_stream)
-
     def upload(self):
+        """H2D of the compact input stream, the rank table and the scalars."""
         p = self.plan
         with self.torch.cuda.stream(self.stream):
-            p.arena[:self.n_persist].copy_(self.host_img, non_blocking=True)
-            p.rank.copy_(self.host_rank, non_blocking=True)
-            p.scal.copy_(self.host_scal, non_blocking=True)
+            self.d_in[:self.n_in].copy_(self.h_in[:self.n_in], non_blocking=True)
+            p.rank.copy_(self.h_rk, non_blocking=True)
+            p.scal.copy_(self.h_sc, non_blocking=True)
+            self.d_px.copy_(self.h_px, non_blocking=True)
+
+    def h2d_bytes(self):
+        return 8 * (self.n_in + self.px.size + self.sc.size) + 4 * self.rk.size
+
+    def d2h_bytes(self):
+        return 8 * (self.n_out + 2) + 4 * self.rk.size
+
+    def restore_device_input(self):
+        """Re-arm a run with the input already resident in HBM (device-side
+        restore of the rank table / power start; the compact input stream in
+        HBM is untouched by a run)."""
+        p = self.plan
+        with self.torch.cuda.stream(self.stream):
+            p.rank.copy_(self.d_rk0, non_blocking=True)
+            p.scal.copy_(self.d_sc0, non_blocking=True)
+            self.d_px.copy_(self.d_px0, non_blocking=True)
+
+    def snapshot_device_input(self):
+        """Keep a device copy of the freshly uploaded run state (call after
+        upload(), before execute())."""
+        with self.torch.cuda.stream(self.stream):
+            self.d_rk0 = self.plan.rank.clone()
+            self.d_sc0 = self.plan.scal.clone()
+            self.d_px0 = self.d_px.clone()
+
+    def _launch(self):
+        self.plan.run(self.stream.cuda_stream)
 
     def execute(self):
         """Run the factorization on the device (graph replay when captured)."""
@@ -191,7 +229,6 @@ class HQREngine(PlanIO):
             self._launch()
             return
         if self.graph is None:
-            # warm the library (function attributes) outside capture, then capture
             self.stream.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=self.stream):
@@ -201,18 +238,24 @@ class HQREngine(PlanIO):
             self.graph.replay()
 
     def download(self):
+        """D2H of the rank table and the compact factor stream."""
         p = self.plan
         with self.torch.cuda.stream(self.stream):
-            self.out_img.copy_(p.arena[:self.n_persist], non_blocking=True)
-            self.out_rank.copy_(p.rank, non_blocking=True)
+            self.h_tot.copy_(p.totals, non_blocking=True)
+            self.h_rk_out.copy_(p.rank, non_blocking=True)
         self.stream.synchronize()
-        if int(self.out_rank.numpy()[self.builder.flag_slot]) != 0:
+        rk = self.h_rk_out.numpy()
+        if int(rk[self.builder.flag_slot]) != 0:
             raise RankCapacityError(f"a truncated rank exceeded the capacity kcap={self.kcap}; "
                                     "retry with a larger kcap")
+        self.n_out = int(self.h_tot.numpy()[1])
+        with self.torch.cuda.stream(self.stream):
+            self.h_out[:self.n_out].copy_(self.d_out[:self.n_out], non_blocking=True)
+        self.stream.synchronize()
 
-    def factors(self, b: int, img=None, rk=None) -> HodlrQRFactors:
-        return PlanIO.factors(self, b, self.out_img.numpy() if img is None else img,
-                              self.out_rank.numpy() if rk is None else rk)
+    def factors(self, b: int, out=None, rk=None) -> HodlrQRFactors:
+        return PlanIO.factors(self, b, self.outbuf if out is None else out,
+                              self.h_rk_out.numpy() if rk is None else rk)
 
     def norm_estimate(self, b: int = 0) -> float:
         """||A_b||_2 estimate of the last run (device power iteration)."""
@@ -224,7 +267,6 @@ class HQREngine(PlanIO):
         self.execute()
         self.download()
         return [self.factors(b) for b in range(self.B)]
-
 
 
 _ENGINES: dict = {}

@@ -38,8 +38,8 @@ NB = 16          # QR panel width (hq_qr.cu)
 GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
 SVD_MAX_N = 4096
 
-R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL = range(5)
-REGION_NAMES = ("persist", "phase", "apply", "trunc", "small")
+R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT = range(7)
+REGION_NAMES = ("persist", "phase", "apply", "trunc", "small", "in", "out")
 
 
 class Buf:
@@ -188,7 +188,7 @@ class Builder:
         self.B = batch
         self.eps, self.absolute = float(eps), bool(absolute)
         self.max_iter, self.tol = max_iter, tol
-        self.bumps = [Bump(r) for r in range(5)]
+        self.bumps = [Bump(r) for r in range(7)]
         self.slots = Slots()
         self.flag_slot = self.slots.take()
         self.power_done = self.slots.take(batch)
@@ -201,6 +201,32 @@ class Builder:
         self.PW = self.bumps[R_PERSIST].alloc(2 * n * batch)
         self.PG = self.bumps[R_PERSIST].alloc(4 * batch)
         self.ops = []
+        self.in_items, self.out_items = self._io_items()
+
+    def _io_items(self):
+        """Compact input/output streams: (arena Buf, rows, Dim cols) in a fixed
+        order; offsets are prefix sums of rows*cols with run-time ranks."""
+        t, lay = self.tree, self.lay
+        ins, outs = [], []
+        nin = nout = 0
+        for b in range(self.B):
+            d = lay.m[b]
+            for lf in t.leaves((0, 0)):
+                nl = t.size[lf]
+                ins.append((d["leafA"][lf], nl, Dim(nl)))
+                outs.append((d["leafA"][lf], nl, Dim(nl)))
+                outs.append((d["leafT"][lf], nl, Dim(nl)))
+            for u in (t.internal_nodes((0, 0)) if t.L > 0 else []):
+                c1, c2 = t.children(u)
+                m1, m2, kc = t.size[c1], t.size[c2], lay.kc[u]
+                ins += [(d["A12U"][u], m1, Dim(kc, d["rA12"][u])), (d["A12V"][u], m2, Dim(kc, d["rA12"][u])),
+                        (d["A21U"][u], m2, Dim(kc, d["rA21"][u])), (d["A21V"][u], m1, Dim(kc, d["rA21"][u]))]
+                outs += [(d["A12U"][u], m1, Dim(kc, d["rA12"][u])), (d["A12V"][u], m2, Dim(kc, d["rA12"][u])),
+                         (d["A21U"][u], m2, Dim(kc, d["rA21"][u])), (d["YV21"][u], m1, Dim(kc, d["rA21"][u])),
+                         (d["T12U"][u], m1, Dim(kc, d["rT12"][u])), (d["T12V"][u], m2, Dim(kc, d["rT12"][u]))]
+        self.bumps[R_IN].alloc(sum(r * c.cap for _, r, c in ins))
+        self.bumps[R_OUT].alloc(sum(r * c.cap for _, r, c in outs))
+        return ins, outs
 
     # ------------------------------------------------------------ primitives
     def _ph(self, n):
@@ -379,6 +405,8 @@ class Builder:
 
     def build(self):
         t = self.tree
+        # restore the input from the compact staging buffer (first op)
+        self.ops.append(("pack_copy", self.in_items, dict(which=1, base=Buf(R_IN, 0), total=0)))
         if not self.absolute:
             self.power_iteration(t.n)
         # left-orthogonalize the a21 blocks of the leftmost spine: the only B
@@ -398,6 +426,8 @@ class Builder:
                                       V=(d["A21V"][u], t.size[c1]), cap=kc, rank_ri=d["rA21"][u]))
             self.trunc(probs)
         self.rec((0, 0))
+        # compact the factors for one device->host copy (last op)
+        self.ops.append(("pack_copy", self.out_items, dict(which=0, base=Buf(R_OUT, 0), total=1)))
         return self
 
     def eps_slot(self, b):
@@ -593,6 +623,7 @@ class CompiledPlan:
         self.arena = torch.zeros(max(acc, 1), dtype=torch.float64, device=device)
         self.rank = torch.zeros(max(builder.slots.n, 1), dtype=torch.int32, device=device)
         self.scal = torch.zeros(max(2 * builder.B, 2), dtype=torch.float64, device=device)
+        self.totals = torch.zeros(2, dtype=torch.int64, device=device)
         base_ptr = self.arena.data_ptr()
         self.bases = bases
         A = lambda buf: _addr(buf, bases, base_ptr)
@@ -666,6 +697,15 @@ class CompiledPlan:
                 self.launch.append((kind, put(pa), put(sa), len(probs), extra))
             elif kind == "power":
                 self.launch.append(("power", None, None, builder.B, extra))
+            elif kind == "pack_copy":
+                it = np.zeros(len(probs), _abi.COPY_ITEM)
+                for i, (buf, rows, cols) in enumerate(probs):
+                    if extra["which"] == 1:
+                        it[i] = (0, A(buf), rows, cols.cap, cols.ri, rows, rows, 0)
+                    else:
+                        it[i] = (A(buf), 0, rows, cols.cap, cols.ri, rows, rows, 0)
+                self.launch.append(("pack_copy", put(it), None, len(probs),
+                                    dict(extra, base_ptr=A(extra["base"]))))
             else:
                 raise ValueError(kind)
         blob = bytearray(max(off, 256))
@@ -702,6 +742,11 @@ class CompiledPlan:
                 rc = lib.hq_leaf_gather(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
             elif kind == "leaf_scatter":
                 rc = lib.hq_leaf_scatter(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
+            elif kind == "pack_copy":
+                rc = lib.hq_pack_offsets(stream_handle, dp + o1, cnt, rk, ex["base_ptr"],
+                                         self.totals.data_ptr() + 8 * ex["total"], ex["which"])
+                _abi.check(rc, "pack_offsets")
+                rc = lib.hq_copy(stream_handle, dp + o1, cnt, rk)
             elif kind == "power":
                 rc = lib.hq_power_step(stream_handle, self.addr(b.PX), self.addr(b.PW), self.addr(b.PG),
                                        b.tree.n, 2 if b.tree.n >= 2 else 1, sc, b.eps, b.tol,
@@ -710,3 +755,68 @@ class CompiledPlan:
 
     def count_kernels(self):
         return len(self.launch)
+
+
+# ---------------------------------------------------------------- accounting
+
+def _dv(d, rk):
+    return d.cap if d.ri < 0 else int(min(max(int(rk[d.ri]), 0), d.cap))
+
+
+def op_flops(kind, probs, rk):
+    """Algorithmic FP64 flops of one op given the final rank table.
+    gemm 2mnk per term; Householder QR 2mk^2 - 2k^3/3 (+ mk^2 when the full
+    compact-WY T is formed); applyQ 4mkc - 2k^2c; Jacobi SVD counted as the
+    R-SVD estimate 6mn^2 + 20n^3 (Golub-Van Loan, Sigma + U1)."""
+    f = 0.0
+    if kind == "gemm":
+        for (c, ldc, m, n, beta, terms) in probs:
+            mm, nn = _dv(m, rk), _dv(n, rk)
+            for t in terms:
+                f += 2.0 * mm * nn * _dv(t[8], rk)
+    elif kind == "qr":
+        for (w, tau, tp, tf, ldw, ldt, m, k) in probs:
+            mm, kk = _dv(m, rk), _dv(k, rk)
+            r = min(mm, kk)
+            f += 2.0 * mm * r * kk - (2.0 / 3.0) * r ** 3 if mm >= kk else 2.0 * mm * mm * kk - (2.0 / 3.0) * mm ** 3
+            if tf is not None:
+                f += mm * r * r
+    elif kind == "applyq":
+        for p in probs:
+            mm, kk, cc = _dv(p[8], rk), _dv(p[9], rk), _dv(p[10], rk)
+            r = min(mm, kk)
+            f += 4.0 * mm * r * cc - 2.0 * r * r * cc
+    elif kind == "svd":
+        for p in probs:
+            mm, nn = _dv(p[4], rk), _dv(p[5], rk)
+            a, b = max(mm, nn), min(mm, nn)
+            f += 6.0 * a * b * b + 20.0 * b ** 3
+    return f
+
+
+def op_bytes(kind, probs, rk):
+    """Compulsory HBM/L2 bytes (read + write once) of data-movement ops."""
+    by = 0.0
+    if kind == "concat":
+        for (dst, dst2, rows, kri, pieces) in probs:
+            k = sum(_dv(d, rk) for _, _, d, _ in pieces)
+            by += 8.0 * rows * k * (3 if dst2 is not None else 2)
+    elif kind == "pack_copy":
+        for (buf, rows, cols) in probs:
+            by += 16.0 * rows * _dv(cols, rk)
+    elif kind in ("leaf_gather", "leaf_scatter"):
+        for (leaf, panel, nl, ldp, slabs, mri) in probs:
+            by += 16.0 * nl * (nl + sum(int(rk[s[4]]) for s in slabs))
+    return by
+
+
+def plan_accounting(builder, rk):
+    """Per-op-kind launches / flops / bytes of a finished run."""
+    acc = {}
+    for kind, probs, extra in builder.ops:
+        a = acc.setdefault(kind, {"launches": 0, "flops": 0.0, "bytes": 0.0})
+        a["launches"] += 1
+        if probs is not None and not (kind == "gemm" and extra.get("skip") is not None):
+            a["flops"] += op_flops(kind, probs, rk)
+            a["bytes"] += op_bytes(kind, probs, rk)
+    return acc

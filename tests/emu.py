@@ -236,6 +236,24 @@ class Emu:
             x[:] = np.linalg.qr(np.array(w))[0]
             self.scal[2 * i] = est
 
+    def pack_copy(self, o1, cnt, ex):
+        items = self.arr(o1, _abi.COPY_ITEM, cnt)
+        base = ex["base_ptr"]
+        off = 0
+        for it in items:
+            cols = self.dim(it["cols"], it["cols_ri"])
+            rows = int(it["rows"])
+            if ex["which"] == 1:
+                src = self.mat(base + 8 * off, rows, rows, cols)
+                dst = self.mat(it["dst"], it["ldd"], rows, cols)
+            else:
+                src = self.mat(it["src"], it["lds"], rows, cols)
+                dst = self.mat(base + 8 * off, rows, rows, cols)
+            if rows and cols:
+                dst[:] = np.array(src)
+            off += rows * cols
+        self.plan.totals.numpy()[ex["total"]] = off
+
     def run(self):
         for kind, o1, o2, cnt, ex in self.plan.launch:
             if kind == "gemm":
@@ -256,6 +274,8 @@ class Emu:
                 self.leaf(o1, o2, cnt, True)
             elif kind == "power":
                 self.power(ex)
+            elif kind == "pack_copy":
+                self.pack_copy(o1, cnt, ex)
             else:
                 raise ValueError(kind)
 
@@ -267,13 +287,19 @@ def emulate(mats, eps, absolute=False, kcap=512):
     from paper_1809_10585_b200.plan import CompiledPlan
     io = PlanIO(mats[0].tree(), len(mats), eps, absolute, kcap)
     plan = CompiledPlan(io.builder, torch.device("cpu"))
+    from paper_1809_10585_b200.plan import R_IN, R_OUT, R_PERSIST
     io.pack(mats)
-    plan.arena.numpy()[:io.n_persist] = io.img
+    A = plan.arena.numpy()
+    ib, ob = plan.bases[R_IN], plan.bases[R_OUT]
+    A[ib:ib + io.n_in] = io.inbuf[:io.n_in]
+    pxo = plan.bases[R_PERSIST] + io.builder.PX.off
+    A[pxo:pxo + io.px.size] = io.px
     plan.rank.numpy()[:] = io.rk
     plan.scal.numpy()[:] = io.sc
     Emu(plan).run()
-    img = plan.arena.numpy()[:io.n_persist].copy()
     rk = plan.rank.numpy().copy()
     if rk[io.builder.flag_slot]:
         raise RuntimeError("rank capacity overflow")
-    return [io.factors(b, img, rk) for b in range(len(mats))], io, plan
+    n_out = int(plan.totals.numpy()[1])
+    out = A[ob:ob + n_out].copy()
+    return [io.factors(b, out, rk) for b in range(len(mats))], io, plan

@@ -1,0 +1,59 @@
+"""Host-side planner checked without a GPU: the packed launch sequence is
+interpreted by the numpy kernel emulator (tests/emu.py) and compared with the
+CPU oracle / reference golden vectors."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from emu import emulate
+from oracle import hqr_oracle as O
+from paper_1809_10585_b200 import gen
+from paper_1809_10585_b200.hodlr import stats, to_dense, validate_structure
+
+CASES = {
+    "random_n256": (lambda: gen.gen_random_hodlr(256, 32, 4, 8.0, seed=0), 1e-10),
+    "illcond_n256": (lambda: gen.gen_illcond_hodlr(256, 32, 4, 8.0, seed=1), 1e-10),
+    "ragged_n200": (lambda: gen.gen_random_hodlr(200, 24, 3, 8.0, seed=2), 1e-12),
+    "leaf_n48": (lambda: gen.gen_random_hodlr(48, 64, 1, 8.0, seed=3), 1e-14),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_plan_matches_golden(name):
+    build, eps = CASES[name]
+    g = load_golden(name)
+    a = build()
+    (f,), io, plan = emulate([a], eps)
+    for h in (f.y, f.t, f.r):
+        validate_structure(h)
+    rd = to_dense(f.r)
+    assert np.linalg.norm(rd - g["R"]) / np.linalg.norm(g["R"]) <= 100 * eps
+    e_orth, e_acc = O.dense_metrics(to_dense(a), f.y, f.t, f.r)
+    assert e_orth <= 10 * max(float(g["e_orth"]), 1e-15)
+    assert e_acc <= 10 * max(float(g["e_acc"]), 1e-15)
+    assert stats(f.r)["max_offdiag_rank"] == int(g["rank_r"])
+    assert stats(f.y)["max_offdiag_rank"] == int(g["rank_y"])
+
+
+def test_plan_batched_matches_single():
+    mats = [gen.gen_random_hodlr(128, 32, 3, 8.0, seed=s) for s in range(3)]
+    fs, io, plan = emulate(mats, 1e-10)
+    for a, f in zip(mats, fs):
+        y, t, r = O.hqr(a, 1e-10)
+        rel = np.linalg.norm(to_dense(f.r) - to_dense(r)) / np.linalg.norm(to_dense(r))
+        assert rel <= 1e-8
+
+
+def test_plan_absolute_eps():
+    a = gen.gen_random_hodlr(128, 32, 3, 8.0, seed=4)
+    (f,), io, plan = emulate([a], 1e-9, absolute=True)
+    y, t, r = O.hqr(a, 1e-9, absolute=True)
+    assert stats(f.r)["max_offdiag_rank"] == stats(r)["max_offdiag_rank"]
+    assert np.linalg.norm(to_dense(f.r) - to_dense(r)) <= 1e-7 * np.linalg.norm(to_dense(r))
+
+
+def test_rank_capacity_overflow_raises():
+    a = gen.gen_random_hodlr(128, 32, 4, 8.0, seed=5)
+    with pytest.raises(Exception):
+        emulate([a], 1e-14, kcap=2)
