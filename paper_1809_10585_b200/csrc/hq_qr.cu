@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
 #pragma unroll
           for (int a = 0; a < NB; ++a) {
             const double v = warp_sum(acc[a]);
-            if (lane == 0) TF[b + (size_t)(p0 + a) * ldt] = v;   // temp: X in place
+            if (lane == 0 && a < pw) TF[b + (size_t)(p0 + a) * ldt] = v;   // temp: X in place
           }
         }
         __syncthreads();

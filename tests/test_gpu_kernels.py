@@ -1,0 +1,127 @@
+"""Each CUDA kernel of libhqb200.so against a numpy statement of its
+contract (include/hodlrqr_b200.h), on odd / ragged / degenerate shapes."""
+
+import numpy as np
+import pytest
+
+from emu import Emu  # noqa: F401  (numpy semantics reference lives in emu)
+from paper_1809_10585_b200 import _abi
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    return torch, _abi.load()
+
+
+def colmajor(torch, a):
+    a = np.asarray(a, dtype=np.float64)
+    return torch.tensor(a.T.copy(), device="cuda").contiguous()  # storage = a in column-major
+
+
+def back(t, rows, cols):
+    return t.cpu().numpy().reshape(cols, rows).T
+
+
+def put(torch, arr):
+    raw = np.frombuffer(arr.tobytes(), np.uint8)
+    return torch.tensor(raw, device="cuda")
+
+
+@pytest.mark.parametrize("m,n,k,ta,tb", [(25, 3, 25, 0, 0), (25, 25, 6, 1, 0), (7, 33, 65, 0, 1),
+                                         (130, 70, 19, 1, 1), (1, 1, 1, 0, 0)])
+def test_gemm(dev, m, n, k, ta, tb):
+    torch, lib = dev
+    rng = np.random.default_rng(m * 100 + n)
+    A = rng.standard_normal((k, m) if ta else (m, k))
+    B = rng.standard_normal((n, k) if tb else (k, n))
+    C = rng.standard_normal((m, n))
+    dA, dB, dC = colmajor(torch, A), colmajor(torch, B), colmajor(torch, C)
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    terms = np.zeros(1, _abi.GEMM_TERM)
+    terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, 0, 0, -0.5)
+    probs = np.zeros(1, _abi.GEMM_PROB)
+    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 1, 0, 2.0)
+    dt, dp = put(torch, terms), put(torch, probs)
+    tiles = -(-m // 64) * -(-n // 64)
+    assert lib.hq_gemm(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), tiles, 1, None) == 0
+    torch.cuda.synchronize()
+    ref = 2.0 * C - 0.5 * ((A.T if ta else A) @ (B.T if tb else B))
+    assert np.allclose(back(dC, m, n), ref, atol=1e-12 * max(1, np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("m,k", [(25, 25), (28, 25), (9, 6), (300, 40), (50, 70), (1200, 17), (200, 200), (60, 57)])
+def test_qr_and_applyq(dev, m, k):
+    torch, lib = dev
+    rng = np.random.default_rng(m + 7 * k)
+    A = rng.standard_normal((m, k))
+    A[:, min(2, k - 1)] = 0.0  # a zero column
+    dW = colmajor(torch, A)
+    r = min(m, k)
+    tau = torch.zeros(max(r, 1), dtype=torch.float64, device="cuda")
+    tp = torch.zeros(((r + 15) // 16) * 256 + 256, dtype=torch.float64, device="cuda")
+    tf = torch.full((r * r + 32 * r,), float("nan"), dtype=torch.float64, device="cuda")
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    q = np.zeros(1, _abi.QR_PROB)
+    q[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), tf.data_ptr(), m, r, m, -1, k, -1)
+    dq = put(torch, q)
+    assert lib.hq_qr(None, dq.data_ptr(), 1, rank.data_ptr()) == 0
+    torch.cuda.synchronize()
+    W = back(dW, m, k)
+    R = np.triu(W[:r])
+    Y = np.tril(W[:, :r], -1)
+    Y[np.arange(r), np.arange(r)] = 1.0
+    assert torch.isnan(tf[r * r:]).all(), "QR wrote past the end of the T factor"
+    T = back(tf[:r * r], r, r)
+    Q = np.eye(m) - Y @ T @ Y.T
+    assert np.linalg.norm(Q.T @ Q - np.eye(m)) <= 1e-13 * m
+    assert np.linalg.norm(Q[:, :r] @ R - A) <= 1e-13 * max(1, np.linalg.norm(A))
+    # reference sign convention: R_jj = -sign(x0) * ||x||
+    from oracle.hqr_oracle import block_qr
+    Yr, Tr, Rr = block_qr(A, 32) if m >= k else (None, None, None)
+    if Rr is not None:
+        assert np.abs(R - Rr).max() <= 1e-11 * max(1, np.abs(Rr).max())
+    # applyq: Q [X0; 0]
+    c = 5
+    X0 = rng.standard_normal((r, c))
+    dX0 = colmajor(torch, X0)
+    dX = torch.zeros(m * c, dtype=torch.float64, device="cuda")
+    ap = np.zeros(1, _abi.APPLYQ_PROB)
+    ap[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), dX.data_ptr(), dX0.data_ptr(), m, m, r,
+             m, -1, k, -1, c, -1, r, -1, 0)
+    da = put(torch, ap)
+    assert lib.hq_applyq(None, da.data_ptr(), 1, rank.data_ptr()) == 0
+    torch.cuda.synchronize()
+    ref = Q[:, :r] @ X0
+    assert np.abs(back(dX, m, c) - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60)])
+def test_svd_truncation(dev, m, n, keep):
+    torch, lib = dev
+    rng = np.random.default_rng(m * n)
+    u = np.linalg.qr(rng.standard_normal((m, min(m, n))))[0]
+    v = np.linalg.qr(rng.standard_normal((n, min(m, n))))[0]
+    s = np.logspace(0, -14, min(m, n))
+    C = (u * s) @ v.T
+    thr = float(s[keep]) * 1.000001 if keep < len(s) else 0.0
+    dC = colmajor(torch, C)
+    dU = torch.zeros(m * min(m, n), dtype=torch.float64, device="cuda")
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    scal = torch.zeros(2, dtype=torch.float64, device="cuda")
+    p = np.zeros(1, _abi.SVD_PROB)
+    p[0] = (dC.data_ptr(), dU.data_ptr(), m, m, m, -1, n, -1, min(m, n), 0, 1, -1, thr)
+    dp = put(torch, p)
+    assert lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr()) == 0
+    torch.cuda.synchronize()
+    k = int(rank[0].item())
+    assert k == min(keep, len(s))
+    U = back(dU, m, min(m, n))[:, :k]
+    assert np.linalg.norm(U.T @ U - np.eye(k)) <= 1e-12 * max(k, 1)
+    # projection error of C onto span(U) equals the dropped tail (<= thr)
+    err = np.linalg.norm(C - U @ (U.T @ C), 2)
+    assert err <= max(thr, 1e-14) * 1.0001 + 1e-14
