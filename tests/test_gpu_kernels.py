@@ -76,7 +76,7 @@ def test_qr_and_applyq(dev, m, k):
     Y = np.tril(W[:, :r], -1)
     Y[np.arange(r), np.arange(r)] = 1.0
     assert torch.isnan(tf[r * r:]).all(), "QR wrote past the end of the T factor"
-    T = back(tf[:r * r], r, r)
+    T = np.triu(np.nan_to_num(back(tf[:r * r], r, r)))
     Q = np.eye(m) - Y @ T @ Y.T
     assert np.linalg.norm(Q.T @ Q - np.eye(m)) <= 1e-13 * m
     assert np.linalg.norm(Q[:, :r] @ R - A) <= 1e-13 * max(1, np.linalg.norm(A))
