@@ -103,18 +103,24 @@ typedef struct hq_applyq_prob {
   int32_t trans;
 } hq_applyq_prob;
 
-/* one-sided Jacobi SVD of C (m x n, destroyed).  Keeps the k' columns with
-   sigma > thr, thr = eps_scale * scal[eps_slot] (eps_slot < 0: eps_scale),
-   writes left singular vectors U_k (m x k', sigma descending) and k' into
-   rank[rank_ri]; k' > cap sets rank[flag_ri] = 1 and clamps
+/* one-sided Jacobi SVD of X (m x n).  xform = 0: X = C as stored (destroyed).
+   xform = 1: c holds R (from hq_qr of C^T, R upper, min(n,m) x m) and
+   X = R^T (m x min(m,n)): the LQ-preconditioned matrix whose left singular
+   vectors are those of C and on which Jacobi converges in a few sweeps.
+   Keeps the k' columns with sigma > thr, thr = eps_scale * scal[eps_slot]
+   (eps_slot < 0: eps_scale), writes the left singular vectors U_k (m x k',
+   sigma descending) and k' into rank[rank_ri]; k' > cap sets rank[flag_ri]
+   and clamps.  work: m*n doubles used when X does not fit shared memory.
    (reference: svd + truncation_rank in core.py:250-253, dense.py:93-99) */
 typedef struct hq_svd_prob {
   double* c;
   double* u;
+  double* work;
   int32_t ldc, ldu;
   int32_t m, m_ri, n, n_ri;
   int32_t cap, rank_ri, flag_ri, eps_slot;
   double eps_scale;
+  int32_t xform, pad_;
 } hq_svd_prob;
 
 /* a slab of reduced-away rows B_R of an ancestor (hqr.py:112,127) */

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhqb200.so")
+LIB_PATH = os.environ.get("HQ_LIB", os.path.join(HERE, "libhqb200.so"))
 
 P = np.uint64  # device pointer
 I = np.int32
@@ -33,9 +33,10 @@ APPLYQ_PROB = np.dtype([("w", P), ("tau", P), ("tpanel", P), ("x", P), ("x0", P)
                         ("ldw", I), ("ldx", I), ("ldx0", I), ("m", I), ("m_ri", I),
                         ("k", I), ("k_ri", I), ("c", I), ("c_ri", I), ("r0", I), ("r0_ri", I),
                         ("trans", I)], align=True)
-SVD_PROB = np.dtype([("c", P), ("u", P), ("ldc", I), ("ldu", I), ("m", I), ("m_ri", I),
-                     ("n", I), ("n_ri", I), ("cap", I), ("rank_ri", I), ("flag_ri", I),
-                     ("eps_slot", I), ("eps_scale", np.float64)], align=True)
+SVD_PROB = np.dtype([("c", P), ("u", P), ("work", P), ("ldc", I), ("ldu", I), ("m", I),
+                     ("m_ri", I), ("n", I), ("n_ri", I), ("cap", I), ("rank_ri", I),
+                     ("flag_ri", I), ("eps_slot", I), ("eps_scale", np.float64),
+                     ("xform", I), ("pad_", I)], align=True)
 SLAB = np.dtype([("v", P), ("yv", P), ("ld", I), ("ldy", I), ("k_ri", I), ("pad_", I)], align=True)
 LEAF_PROB = np.dtype([("leaf", P), ("panel", P), ("nl", I), ("ldp", I), ("slab0", I),
                       ("nslab", I), ("m_ri", I), ("pad_", I)], align=True)

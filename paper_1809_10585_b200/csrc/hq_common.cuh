@@ -45,3 +45,11 @@ HQ_DEV double hq_mask(double v, int r, int c, int mask) {
 }
 
 static inline int hq_err(cudaError_t e) { return (int)e; }
+
+// D (8x8, 2 per lane) += A (8x4, 1 per lane) * B (4x8, 1 per lane): FP64 DMMA.
+// Lane l holds A[l>>2][l&3], B[l&3][l>>2], D[l>>2][2(l&3) + {0,1}].
+HQ_DEV void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}

@@ -11,7 +11,8 @@
 namespace {
 constexpr int NT = 256, NW = NT / 32, NB = 16;
 constexpr int STAGE_ROWS = 1024;  // panel staged in smem when rows <= STAGE_ROWS
-constexpr int CW = 32;            // trailing-update column chunk
+constexpr int CW = 64;            // trailing-update column chunk
+constexpr int MAXK_T = 512;       // max columns when the full compact-WY T is formed
 
 struct QrSmem {
   double panel[STAGE_ROWS * NB];
@@ -21,6 +22,7 @@ struct QrSmem {
   double tcol[NB];
   double wc[NB * CW];
   double wc2[NB * CW];
+  double xs[MAXK_T * NB];   // X = Y[:,0:p0]^T Y_p, then X T_p (full-T merge)
   double red[32];
   double scal[4];
 };
@@ -96,46 +98,67 @@ __device__ __forceinline__ double yval(const double* P, int ldp, int i, int a) {
   return i == a ? 1.0 : (i > a ? P[i + (size_t)a * ldp] : 0.0);
 }
 
-// W_blk (rows x cw at col) -= Y (T^op (Y^T W_blk)); Y = panel reflectors
-// (rows x pw, local diag at a), tp its T.  trans_t: use T^T (Q^T) else T (Q).
+// X (rows x ncols) := (I - Y T^op Y^T) X for panel reflectors Y (rows x pw,
+// unit diagonal at local row a; smem or global) with T factor tp (NB x NB).
+// trans_t: T^T (applies Q^T) else T (applies Q).  Both products run on the
+// FP64 tensor pipe (mma.sync m8n8k4): W = Y^T X (16 x CW), W2 = T^op W,
+// X -= Y W2, column chunks of CW.
 __device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, const double* tp,
                                  double* X, int ldx, int ncols, bool trans_t, QrSmem& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
   for (int c0 = 0; c0 < ncols; c0 += CW) {
     const int cw = min(CW, ncols - c0);
-    for (int cc = wid; cc < cw; cc += NW) {
-      const double* col = X + (size_t)(c0 + cc) * ldx;
-      double acc[NB];
-#pragma unroll
-      for (int a = 0; a < NB; ++a) acc[a] = 0.0;
-      for (int i = lane; i < rows; i += 32) {
-        const double x = col[i];
-#pragma unroll
-        for (int a = 0; a < NB; ++a)
-          if (a < pw) acc[a] = fma(yval(Y, ldy, i, a), x, acc[a]);
+    // ---- W = Y^T X_chunk : 2 x (CW/8) output tiles of 8x8
+    for (int tile = wid; tile < 2 * (CW / 8); tile += NW) {
+      const int mt = tile & 1, nt = tile >> 1;
+      if (nt * 8 >= cw) continue;
+      double d0 = 0.0, d1 = 0.0;
+      const int a = mt * 8 + gq;          // A row  (reflector index)
+      const int j = nt * 8 + gq;          // B col  (chunk column)
+      const double* xc = X + (size_t)(c0 + j) * ldx;
+      for (int k0 = 0; k0 < rows; k0 += 4) {
+        const int ia = k0 + tq;           // A col / B row (matrix row)
+        const double av = (ia < rows && a < pw) ? yval(Y, ldy, ia, a) : 0.0;
+        const double bv = (ia < rows && j < cw) ? xc[ia] : 0.0;
+        dmma884(d0, d1, av, bv);
       }
-#pragma unroll
-      for (int a = 0; a < NB; ++a) {
-        const double v = warp_sum(acc[a]);
-        if (lane == 0) S.wc[a + cc * NB] = v;
-      }
+      const int r = mt * 8 + gq, cc = nt * 8 + 2 * tq;
+      S.wc[r + cc * NB] = d0;
+      S.wc[r + (cc + 1) * NB] = d1;
     }
     __syncthreads();
-    for (int e = t; e < pw * cw; e += NT) {
-      const int a = e % pw, cc = e / pw;
+    for (int e = t; e < NB * cw; e += NT) {
+      const int a = e % NB, cc = e / NB;
       double v = 0.0;
-      if (trans_t) { for (int b = 0; b <= a; ++b) v = fma(tp[b + a * NB], S.wc[b + cc * NB], v); }
-      else { for (int b = a; b < pw; ++b) v = fma(tp[a + b * NB], S.wc[b + cc * NB], v); }
+      if (a < pw) {
+        if (trans_t) { for (int b = 0; b <= a; ++b) v = fma(tp[b + a * NB], S.wc[b + cc * NB], v); }
+        else { for (int b = a; b < pw; ++b) v = fma(tp[a + b * NB], S.wc[b + cc * NB], v); }
+      }
       S.wc2[a + cc * NB] = v;
     }
     __syncthreads();
-    for (int cc = wid; cc < cw; cc += NW) {
-      double* col = X + (size_t)(c0 + cc) * ldx;
-      for (int i = lane; i < rows; i += 32) {
-        double v = col[i];
-        for (int a = 0; a < pw; ++a) v = fma(-yval(Y, ldy, i, a), S.wc2[a + cc * NB], v);
-        col[i] = v;
+    // ---- X_chunk -= Y W2 : (rows/8) x (cw/8) tiles, k = NB
+    const int ntm = (rows + 7) / 8, ntn = (cw + 7) / 8;
+    for (int tile = wid; tile < ntm * ntn; tile += NW) {
+      const int mt = tile % ntm, nt = tile / ntm;
+      const int i = mt * 8 + gq;              // output row
+      const int j = nt * 8 + 2 * tq;          // output cols j, j+1
+      double* x0 = X + (size_t)(c0 + j) * ldx;
+      double* x1 = x0 + ldx;
+      double d0 = (i < rows && j < cw) ? x0[i] : 0.0;
+      double d1 = (i < rows && j + 1 < cw) ? x1[i] : 0.0;
+      const int ib = mt * 8 + gq;             // A row for the fragment
+      const int jb = nt * 8 + gq;             // B col for the fragment
+#pragma unroll
+      for (int k0 = 0; k0 < NB; k0 += 4) {
+        const int a = k0 + tq;
+        const double av = (ib < rows && a < pw) ? -yval(Y, ldy, ib, a) : 0.0;
+        const double bv = (jb < cw) ? S.wc2[a + jb * NB] : 0.0;
+        dmma884(d0, d1, av, bv);
       }
+      if (i < rows && j < cw) x0[i] = d0;
+      if (i < rows && j + 1 < cw) x1[i] = d1;
     }
     __syncthreads();
   }
@@ -176,56 +199,54 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
     if (Q.tfull) {
       double* TF = Q.tfull;
       const int ldt = Q.ldt;
+      const int gq = lane >> 2, tq = lane & 3;
       for (int e = t; e < pw * pw; e += NT) TF[(p0 + e % pw) + (size_t)(p0 + e / pw) * ldt] = S.tp[e % pw + (e / pw) * NB];
-      for (int e = t; e < pw * p0; e += NT) TF[(e % p0) + (size_t)(p0 + e / p0) * ldt] = 0.0;
-      __syncthreads();
       if (p0 > 0) {
-        // X = Y[:,0:p0]^T Y_p, b = row (previous reflector), a = panel reflector
-        for (int b = wid; b < p0; b += NW) {
-          double acc[NB];
-#pragma unroll
-          for (int a = 0; a < NB; ++a) acc[a] = 0.0;
-          for (int i = lane; i < rows; i += 32) {
-            const double yb = W[(p0 + i) + (size_t)b * ld];   // p0+i > b: stored reflector
-#pragma unroll
-            for (int a = 0; a < NB; ++a)
-              if (a < pw) acc[a] = fma(yb, yval(Pg, ld, i, a), acc[a]);
+        // X (p0 x NB) = Y[:,0:p0]^T Y_p over local rows 0..rows-1 (DMMA)
+        const int ntm = (p0 + 7) / 8;
+        for (int tile = wid; tile < ntm * 2; tile += NW) {
+          const int mt = tile >> 1, nt = tile & 1;
+          const int b = mt * 8 + gq, a = nt * 8 + gq;
+          double d0 = 0.0, d1 = 0.0;
+          for (int k0 = 0; k0 < rows; k0 += 4) {
+            const int i = k0 + tq;
+            const double av = (i < rows && b < p0) ? W[(p0 + i) + (size_t)b * ld] : 0.0;
+            const double bv = (i < rows && a < pw) ? yval(Pg, ld, i, a) : 0.0;
+            dmma884(d0, d1, av, bv);
           }
+          const int r = mt * 8 + gq, c = nt * 8 + 2 * tq;
+          if (r < p0) { S.xs[r + c * MAXK_T] = d0; S.xs[r + (c + 1) * MAXK_T] = d1; }
+        }
+        __syncthreads();
+        // X := X T_p (in place per row)
+        for (int b = t; b < p0; b += NT) {
+          double xr[NB];
+#pragma unroll
+          for (int a = 0; a < NB; ++a) xr[a] = a < pw ? S.xs[b + a * MAXK_T] : 0.0;
 #pragma unroll
           for (int a = 0; a < NB; ++a) {
-            const double v = warp_sum(acc[a]);
-            if (lane == 0 && a < pw) TF[b + (size_t)(p0 + a) * ldt] = v;   // temp: X in place
-          }
-        }
-        __syncthreads();
-        // X := X T_p (p0 x pw), row by row in registers
-        for (int b = t; b < p0; b += NT) {
-          double xr[NB], out[NB];
-          for (int a = 0; a < pw; ++a) xr[a] = TF[b + (size_t)(p0 + a) * ldt];
-          for (int a = 0; a < pw; ++a) {
             double v = 0.0;
-            for (int c = 0; c <= a; ++c) v = fma(xr[c], S.tp[c + a * NB], v);
-            out[a] = v;
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+              if (c <= a) v = fma(xr[c], S.tp[c + a * NB], v);
+            if (a < pw) S.xs[b + a * MAXK_T] = v;
           }
-          for (int a = 0; a < pw; ++a) TF[b + (size_t)(p0 + a) * ldt] = out[a];
         }
         __syncthreads();
-        // T12 = -T11 X  (T11 upper p0 x p0); rows processed top-down in place is
-        // safe since row b only reads rows >= b of X: do bottom-up
-        for (int a = 0; a < pw; ++a) {
-          double* xc = TF + (size_t)(p0 + a) * ldt;
-          // y_b = -sum_{c>=b} T11[b,c] x_c ; compute into registers by thread per b
-          double v[4] = {0, 0, 0, 0};
-          int nb = 0;
-          for (int b = t; b < p0 && nb < 4; b += NT, ++nb) {
-            double s = 0.0;
-            for (int c = b; c < p0; ++c) s = fma(TF[b + (size_t)c * ldt], xc[c], s);
-            v[nb] = -s;
+        // T[0:p0, p0:p0+pw] = -T11 X   (T11 upper, p0 x p0, read from TF; DMMA)
+        for (int tile = wid; tile < ntm * 2; tile += NW) {
+          const int mt = tile >> 1, nt = tile & 1;
+          const int r = mt * 8 + gq, a = nt * 8 + gq;
+          double d0 = 0.0, d1 = 0.0;
+          for (int k0 = (mt * 8) & ~3; k0 < p0; k0 += 4) {
+            const int c = k0 + tq;
+            const double av = (r < p0 && c < p0 && c >= r) ? -TF[r + (size_t)c * ldt] : 0.0;
+            const double bv = (c < p0 && a < pw) ? S.xs[c + a * MAXK_T] : 0.0;
+            dmma884(d0, d1, av, bv);
           }
-          __syncthreads();
-          nb = 0;
-          for (int b = t; b < p0 && nb < 4; b += NT, ++nb) xc[b] = v[nb];
-          __syncthreads();
+          const int ro = mt * 8 + gq, co = nt * 8 + 2 * tq;
+          if (ro < p0 && co < pw) TF[ro + (size_t)(p0 + co) * ldt] = d0;
+          if (ro < p0 && co + 1 < pw) TF[ro + (size_t)(p0 + co + 1) * ldt] = d1;
         }
       }
       __syncthreads();

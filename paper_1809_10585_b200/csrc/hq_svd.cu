@@ -9,118 +9,9 @@
 // right factor as U_k^T-projections (no division by sigma), see plan.py.
 #include "hq_common.cuh"
 
+#include "hq_svd_kernel.cuh"
+
 namespace {
-constexpr int NT = 256, NW = NT / 32;
-constexpr int SMEM_DOUBLES = 23552;  // 184 KB: C staged in smem when m*n fits
-constexpr int MAX_N = 4096;          // max columns (sigma table)
-constexpr int MAX_SWEEPS = 40;
-
-struct SvdSmem {
-  double cs[SMEM_DOUBLES];
-  double sig[MAX_N];
-  int rot;
-  int cnt;
-};
-
-__global__ void __launch_bounds__(NT) svd_kernel(const hq_svd_prob* __restrict__ probs,
-                                                 int* __restrict__ rank,
-                                                 const double* __restrict__ scal) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SvdSmem& S = *reinterpret_cast<SvdSmem*>(smem_raw);
-  const hq_svd_prob P = probs[blockIdx.x];
-  const int m = hq_dim(rank, P.m, P.m_ri);
-  const int n = min(hq_dim(rank, P.n, P.n_ri), MAX_N);
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  const double thr = P.eps_scale * (P.eps_slot >= 0 ? scal[P.eps_slot] : 1.0);
-  if (m <= 0 || n <= 0) {
-    if (t == 0) rank[P.rank_ri] = 0;
-    return;
-  }
-  double* C = P.c;
-  int ld = P.ldc;
-  const bool staged = (size_t)m * n <= SMEM_DOUBLES;
-  if (staged) {
-    for (int e = t; e < m * n; e += NT) S.cs[e] = C[e % m + (size_t)(e / m) * ld];
-    C = S.cs; ld = m;
-  }
-  __syncthreads();
-  const double tol = sqrt((double)m) * 2.220446049250313e-16;
-  const double tiny = 1e-2 * thr;
-  const int np = n + (n & 1), N = np - 1;  // circle method: N odd, index N fixed
-  for (int sweep = 0; sweep < MAX_SWEEPS && N > 0; ++sweep) {
-    if (t == 0) S.rot = 0;
-    __syncthreads();
-    for (int r = 0; r < N; ++r) {
-      for (int pi = wid; pi < np / 2; pi += NW) {
-        int p, q;
-        if (pi == 0) { p = r; q = N; }
-        else { p = (r + pi) % N; q = (r - pi + N) % N; }
-        if (p >= n || q >= n) continue;
-        if (p > q) { const int tmp = p; p = q; q = tmp; }
-        double* cp = C + (size_t)p * ld;
-        double* cq = C + (size_t)q * ld;
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (int i = lane; i < m; i += 32) {
-          const double x = cp[i], y = cq[i];
-          a = fma(x, x, a); b = fma(y, y, b); g = fma(x, y, g);
-        }
-        a = warp_sum(a); b = warp_sum(b); g = warp_sum(g);
-        const double sa = sqrt(a), sb = sqrt(b);
-        if (g == 0.0 || fabs(g) <= tol * sa * sb) continue;
-        if (sa < tiny && sb < tiny) continue;  // both far below threshold: dropped anyway
-        const double zeta = (b - a) / (2.0 * g);
-        double tt;
-        if (fabs(zeta) > 1e150) tt = 0.5 / zeta;
-        else tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / sqrt(1.0 + tt * tt), s = c * tt;
-        for (int i = lane; i < m; i += 32) {
-          const double x = cp[i], y = cq[i];
-          cp[i] = c * x - s * y;
-          cq[i] = s * x + c * y;
-        }
-        if (lane == 0) S.rot = 1;
-      }
-      __syncthreads();
-    }
-    if (S.rot == 0) break;
-    __syncthreads();
-  }
-  // singular values = column norms
-  for (int j = wid; j < n; j += NW) {
-    const double* cj = C + (size_t)j * ld;
-    double s = 0.0;
-    for (int i = lane; i < m; i += 32) s = fma(cj[i], cj[i], s);
-    s = sqrt(warp_sum(s));
-    if (lane == 0) S.sig[j] = s;
-  }
-  if (t == 0) S.cnt = 0;
-  __syncthreads();
-  // keep sigma > thr (ties truncate), ordered by descending sigma (ties by index)
-  for (int j = wid; j < n; j += NW) {
-    const double s = S.sig[j];
-    if (!(s > thr)) continue;
-    int pos = 0;
-    for (int o = lane; o < n; o += 32) {
-      const double so = S.sig[o];
-      pos += (so > s || (so == s && o < j)) ? 1 : 0;
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
-    if (lane == 0) atomicAdd(&S.cnt, 1);
-    if (pos < P.cap) {
-      const double inv = 1.0 / s;
-      const double* cj = C + (size_t)j * ld;
-      for (int i = lane; i < m; i += 32) P.u[i + (size_t)pos * P.ldu] = cj[i] * inv;
-    }
-  }
-  __syncthreads();
-  if (t == 0) {
-    int kk = S.cnt;
-    if (kk > P.cap) { if (P.flag_ri >= 0) rank[P.flag_ri] = 1; kk = P.cap; }
-    rank[P.rank_ri] = kk;
-  }
-}
-
 // One iteration tail of the two-vector power method (dense.py:121-141) for a
 // batch of matrices (block b <-> matrix b): g = Y^T Y (ncol x ncol), x and
 // w = A^T A x are n x ncol (ld = n), strided by 2n per matrix.

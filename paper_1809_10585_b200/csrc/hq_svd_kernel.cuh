@@ -1,0 +1,309 @@
+// Hestenes one-sided Jacobi (included by hq_svd.cu).
+// Per round of the round-robin schedule: (A) one warp per pair computes the
+// column dot product g, (B) one thread per pair turns (a, b, g) into the
+// rotation (scalar work done once per pair, not 32x), (C) one warp per pair
+// rotates the two columns and updates the carried squared norms.
+namespace {
+constexpr int NT = 512, NW = NT / 32;
+constexpr int SMEM_DOUBLES = 24576;  // 192 KB: X staged in smem when m*n fits
+constexpr int MAX_N = 1024;
+constexpr int MAX_SWEEPS = 40;
+
+struct SvdSmem {
+  double cs[SMEM_DOUBLES];
+  double nrm[MAX_N];
+  double g[MAX_N / 2];
+  double rc[MAX_N / 2];
+  double rs[MAX_N / 2];
+  double rt[MAX_N / 2];
+  int rot;
+  int cnt;
+};
+
+__device__ __forceinline__ void pair_of(int r, int pi, int N, int& p, int& q) {
+  if (pi == 0) { p = r; q = N; }
+  else { p = (r + pi) % N; q = (r - pi + N) % N; }
+  if (p > q) { const int x = p; p = q; q = x; }
+}
+
+// One-sided Jacobi with each pair owned by a group of LP lanes holding both
+// columns in registers (E = m / LP <= 16 doubles per lane per column): one
+// smem read and one smem write of each column per round, dot product reduced
+// with log2(LP) shuffles, the rotation parameters computed by the group.
+template <int LP, bool SMEM>
+__device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, double tiny2, double thr,
+                             SvdSmem& S) {
+  // SMEM: index the staged copy through S.cs so the compiler emits LDS/STS
+  double* X = SMEM ? S.cs : Xg;
+  constexpr int E = 16, GPW = 32 / LP;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int grp = wid * GPW + lane / LP, gl = lane % LP;
+  const int ngroups = NW * GPW;
+  const int np = n + (n & 1), N = np - 1, npair = np / 2;
+  int sweep = 0;
+  for (; sweep < MAX_SWEEPS && N > 0; ++sweep) {
+    for (int j = wid; j < n; j += NW) {
+      const double* xj = X + (size_t)j * ld;
+      double v = 0.0;
+      for (int i = lane; i < m; i += 32) v = fma(xj[i], xj[i], v);
+      v = warp_sum(v);
+      if (lane == 0) S.nrm[j] = v;
+    }
+    if (t == 0) S.rot = 0;
+    __syncthreads();
+    for (int r = 0; r < N; ++r) {
+      for (int pi0 = 0; pi0 < npair; pi0 += ngroups) {
+        const int pi = pi0 + grp;
+        int p = 0, q = n;
+        if (pi < npair) pair_of(r, pi, N, p, q);
+        const bool act = pi < npair && q < n;
+        double a = 0.0, b = 0.0;
+        if (act) { a = S.nrm[p]; b = S.nrm[q]; }
+        const bool work = act && !(a + b < thr * thr) && !(a < tiny2 && b < tiny2);
+        double xp[E], xq[E];
+        double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+        double* cp = X + (size_t)p * ld;
+        double* cq = X + (size_t)(work ? q : p) * ld;
+        if (SMEM) {
+          // lane gl owns rows 2gl + 2LP e + {0,1}: a group reads 16 B x LP
+          // contiguous bytes per load -> conflict-free 128-bit shared loads
+#pragma unroll
+          for (int e = 0; e < E / 2; ++e) {
+            const int i = 2 * gl + 2 * LP * e;
+            double2 vp = make_double2(0.0, 0.0), vq = make_double2(0.0, 0.0);
+            if (work && i < ld) {
+              vp = *reinterpret_cast<const double2*>(cp + i);
+              vq = *reinterpret_cast<const double2*>(cq + i);
+            }
+            xp[2 * e] = vp.x; xp[2 * e + 1] = vp.y;
+            xq[2 * e] = vq.x; xq[2 * e + 1] = vq.y;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; ++e) {
+            const int i = gl + e * LP;
+            xp[e] = (work && i < m) ? cp[i] : 0.0;
+            xq[e] = (work && i < m) ? cq[i] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+          g0 = fma(xp[e], xq[e], g0);
+          g1 = fma(xp[e + 1], xq[e + 1], g1);
+          g2 = fma(xp[e + 2], xq[e + 2], g2);
+          g3 = fma(xp[e + 3], xq[e + 3], g3);
+        }
+        double g = (g0 + g1) + (g2 + g3);
+#pragma unroll
+        for (int o = LP / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+        bool rot = work && g != 0.0 && g * g > (tol * tol) * (a * b);
+        double c = 1.0, sn = 0.0, tt = 0.0;
+        if (rot) {
+          // tangent of the rotation angle: any t gives an exactly orthogonal
+          // rotation once c = (1+t^2)^(-1/2) is accurate, so t is formed in
+          // single precision when in range (costs at most one extra sweep)
+          const double zeta = (b - a) / (2.0 * g);
+          if (fabs(zeta) < 1e18) {
+            const float zf = (float)zeta;
+            tt = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
+          } else {
+            tt = 0.5 / zeta;
+          }
+          c = rsqrt(1.0 + tt * tt);
+          sn = c * tt;
+          if (SMEM) {
+#pragma unroll
+            for (int e = 0; e < E / 2; ++e) {
+              const int i = 2 * gl + 2 * LP * e;
+              if (i < ld) {
+                *reinterpret_cast<double2*>(cp + i) =
+                    make_double2(c * xp[2 * e] - sn * xq[2 * e], c * xp[2 * e + 1] - sn * xq[2 * e + 1]);
+                *reinterpret_cast<double2*>(cq + i) =
+                    make_double2(sn * xp[2 * e] + c * xq[2 * e], sn * xp[2 * e + 1] + c * xq[2 * e + 1]);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+              const int i = gl + e * LP;
+              if (i < m) {
+                const double x = xp[e], y = xq[e];
+                cp[i] = c * x - sn * y;
+                cq[i] = sn * x + c * y;
+              }
+            }
+          }
+          if (gl == 0) {
+            S.nrm[p] = fmax(a - tt * g, 0.0);
+            S.nrm[q] = b + tt * g;
+            S.rot = 1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (S.rot == 0) { ++sweep; break; }
+    __syncthreads();
+  }
+  return sweep;
+}
+
+__global__ void __launch_bounds__(NT, 1) svd_kernel(const hq_svd_prob* __restrict__ probs,
+                                                    int* __restrict__ rank,
+                                                    const double* __restrict__ scal) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SvdSmem& S = *reinterpret_cast<SvdSmem*>(smem_raw);
+  const hq_svd_prob P = probs[blockIdx.x];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int m = hq_dim(rank, P.m, P.m_ri);
+  int n = hq_dim(rank, P.n, P.n_ri);
+  if (P.xform) n = min(n, m);
+  const double thr = P.eps_scale * (P.eps_slot >= 0 ? scal[P.eps_slot] : 1.0);
+  if (t == 0 && P.flag_ri >= 0 && (n > MAX_N || (P.n >= MAX_N && P.n_ri >= 0 && rank[P.n_ri] > P.n)))
+    rank[P.flag_ri] = 1;
+  n = min(n, MAX_N);
+  if (m <= 0 || n <= 0) {
+    if (t == 0) rank[P.rank_ri] = 0;
+    return;
+  }
+  const int lds = (m + 1) & ~1;  // even leading dim: 16 B aligned columns for double2
+  const bool staged = (size_t)lds * n <= SMEM_DOUBLES;
+  double* X;
+  int ld;
+  if (staged) { X = S.cs; ld = lds; }
+  else if (P.xform) { X = P.work; ld = m; }
+  else { X = P.c; ld = P.ldc; }
+  if (P.xform) {
+    // X[i][j] = R[j][i] (j <= i), R stored in c with leading dim ldc
+    for (int e = t; e < m * n; e += NT) {
+      const int i = e % m, j = e / m;
+      X[i + (size_t)j * ld] = j <= i ? P.c[j + (size_t)i * P.ldc] : 0.0;
+    }
+  } else if (staged) {
+    for (int e = t; e < m * n; e += NT) X[e % m + (size_t)(e / m) * ld] = P.c[e % m + (size_t)(e / m) * P.ldc];
+  }
+  if (staged && lds != m)
+    for (int j = t; j < n; j += NT) X[m + (size_t)j * ld] = 0.0;
+  __syncthreads();
+  const double tol = 4.0 * sqrt((double)m) * 2.220446049250313e-16;
+  const double tiny2 = (1e-3 * thr) * (1e-3 * thr);
+  const int np = n + (n & 1), N = np - 1, npair = np / 2;
+  int nsweeps = 0;
+  if (m <= 512) {
+    // register-cached path: a group of LP lanes owns a pair (E <= 16 rows per lane)
+    if (staged) {
+      if (m <= 128) nsweeps = jacobi_groups<8, true>(X, ld, m, n, tol, tiny2, thr, S);
+      else if (m <= 256) nsweeps = jacobi_groups<16, true>(X, ld, m, n, tol, tiny2, thr, S);
+      else nsweeps = jacobi_groups<32, true>(X, ld, m, n, tol, tiny2, thr, S);
+    } else {
+      if (m <= 128) nsweeps = jacobi_groups<8, false>(X, ld, m, n, tol, tiny2, thr, S);
+      else if (m <= 256) nsweeps = jacobi_groups<16, false>(X, ld, m, n, tol, tiny2, thr, S);
+      else nsweeps = jacobi_groups<32, false>(X, ld, m, n, tol, tiny2, thr, S);
+    }
+  }
+  for (int sweep = 0; sweep < MAX_SWEEPS && N > 0 && !(m <= 512); ++sweep) {
+    nsweeps = sweep + 1;
+    for (int j = wid; j < n; j += NW) {
+      const double* xj = X + (size_t)j * ld;
+      double v = 0.0;
+      for (int i = lane; i < m; i += 32) v = fma(xj[i], xj[i], v);
+      v = warp_sum(v);
+      if (lane == 0) S.nrm[j] = v;
+    }
+    if (t == 0) S.rot = 0;
+    __syncthreads();
+    for (int r = 0; r < N; ++r) {
+      // (A) dot products
+      for (int pi = wid; pi < npair; pi += NW) {
+        int p, q;
+        pair_of(r, pi, N, p, q);
+        double g = 0.0;
+        if (q < n && !(S.nrm[p] < tiny2 && S.nrm[q] < tiny2)) {
+          const double* xp = X + (size_t)p * ld;
+          const double* xq = X + (size_t)q * ld;
+          for (int i = lane; i < m; i += 32) g = fma(xp[i], xq[i], g);
+          g = warp_sum(g);
+        }
+        if (lane == 0) S.g[pi] = g;
+      }
+      __syncthreads();
+      // (B) rotation parameters, one thread per pair
+      for (int pi = t; pi < npair; pi += NT) {
+        int p, q;
+        pair_of(r, pi, N, p, q);
+        double c = 1.0, sn = 0.0, tt = 0.0;
+        const double g = S.g[pi];
+        if (q < n && g != 0.0) {
+          const double a = S.nrm[p], b = S.nrm[q];
+          if (fabs(g) > tol * sqrt(a * b)) {
+            const double zeta = (b - a) / (2.0 * g);
+            tt = fabs(zeta) > 1e150 ? 0.5 / zeta
+                                    : (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            c = rsqrt(1.0 + tt * tt);
+            sn = c * tt;
+            S.nrm[p] = fmax(a - tt * g, 0.0);
+            S.nrm[q] = b + tt * g;
+            S.rot = 1;
+          }
+        }
+        S.rc[pi] = c; S.rs[pi] = sn; S.rt[pi] = tt;
+      }
+      __syncthreads();
+      // (C) rotations
+      for (int pi = wid; pi < npair; pi += NW) {
+        if (S.rt[pi] == 0.0) continue;
+        int p, q;
+        pair_of(r, pi, N, p, q);
+        const double c = S.rc[pi], sn = S.rs[pi];
+        double* xp = X + (size_t)p * ld;
+        double* xq = X + (size_t)q * ld;
+        for (int i = lane; i < m; i += 32) {
+          const double x = xp[i], y = xq[i];
+          xp[i] = c * x - sn * y;
+          xq[i] = sn * x + c * y;
+        }
+      }
+      __syncthreads();
+    }
+    if (S.rot == 0) break;
+    __syncthreads();
+  }
+  // singular values = exact column norms
+  for (int j = wid; j < n; j += NW) {
+    const double* xj = X + (size_t)j * ld;
+    double v = 0.0;
+    for (int i = lane; i < m; i += 32) v = fma(xj[i], xj[i], v);
+    v = sqrt(warp_sum(v));
+    if (lane == 0) S.nrm[j] = v;
+  }
+  if (t == 0) S.cnt = 0;
+  __syncthreads();
+  for (int j = wid; j < n; j += NW) {
+    const double sj = S.nrm[j];
+    if (!(sj > thr)) continue;
+    int pos = 0;
+    for (int o = lane; o < n; o += 32) {
+      const double so = S.nrm[o];
+      pos += (so > sj || (so == sj && o < j)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
+    if (lane == 0) atomicAdd(&S.cnt, 1);
+    if (pos < P.cap) {
+      const double inv = 1.0 / sj;
+      const double* xj = X + (size_t)j * ld;
+      for (int i = lane; i < m; i += 32) P.u[i + (size_t)pos * P.ldu] = xj[i] * inv;
+    }
+  }
+  __syncthreads();
+  if (t == 0) {
+    int kk = S.cnt;
+    if (kk > P.cap) { if (P.flag_ri >= 0) rank[P.flag_ri] = 1; kk = P.cap; }
+    rank[P.rank_ri] = kk;
+#ifdef HQ_DEBUG_SWEEPS
+    if (P.flag_ri >= 0) rank[P.flag_ri + 1] = nsweeps;
+#endif
+  }
+  (void)nsweeps;
+}
+}  // namespace

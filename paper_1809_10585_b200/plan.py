@@ -36,7 +36,7 @@ from .hodlr import PartitionTree
 
 NB = 16          # QR panel width (hq_qr.cu)
 GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
-SVD_MAX_N = 4096
+SVD_MAX_N = 1024
 
 R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT = range(7)
 REGION_NAMES = ("persist", "phase", "apply", "trunc", "small", "in", "out")
@@ -333,30 +333,34 @@ class Builder:
             return
         z = self.bumps[R_TRUNC]
         z.reset()
-        cat, cat_pieces, qr, gm_c, svd, apq, gm_m, gm_v = [], [], [], [], [], [], [], []
+        cat, cat_pieces, qr, gm_c, qrc, svd, apq, gm_m, gm_v = [], [], [], [], [], [], [], [], []
         maxrows = 0
         for p in probs:
             m, n, cap = p["m"], p["n"], p["cap"]
             kcap = sum(d.cap for _, _, d, _ in p["L"])
             assert kcap == sum(d.cap for _, _, d, _ in p["R"]), "L/R piece capacities differ"
-            k1, k2 = min(m, kcap), min(n, kcap)
-            assert k2 <= SVD_MAX_N, "truncation core too wide"
+            k1, k2 = min(m, kcap), min(n, kcap, SVD_MAX_N)
             WL, WR, WRc = z.alloc(m * kcap), z.alloc(n * kcap), z.alloc(n * kcap)
             tauL, tauR = z.alloc(kcap), z.alloc(kcap)
             npan = max(1, math.ceil(kcap / NB))
             tpL, tpR = z.alloc(npan * NB * NB), z.alloc(npan * NB * NB)
             C, Uk, Mm = z.alloc(k1 * k2), z.alloc(k1 * cap), z.alloc(kcap * cap)
+            Xw = z.alloc(k1 * min(k1, k2))
+            tauC = z.alloc(min(k1, k2))
+            tpC = z.alloc(max(1, math.ceil(min(k1, k2) / NB)) * NB * NB)
             kL, kR = self.slots.take(), self.slots.take()
             cat.append((WL, None, m, kL, p["L"]))
             cat.append((WR, WRc, n, kR, p["R"]))
             maxrows = max(maxrows, m, n)
             qr.append((WL, tauL, tpL, None, m, 0, Dim(m), Dim(kcap, kL)))
             qr.append((WR, tauR, tpR, None, n, 0, Dim(n), Dim(kcap, kR)))
-            # C = R1 R2^T (masks: upper on the stored R factors)
-            gm_c.append((C, k1, Dim(k1, kL), Dim(k2, kR), 0.0,
-                         [(WL, m, 0, 1, WR, n, 1, 1, Dim(kcap, kL), 1.0)]))
-            svd.append((C, Uk, k1, k1, Dim(k1, kL), Dim(k2, kR), cap, p["rank_ri"],
-                        self.flag_slot, p["eps_slot"], p["eps_scale"]))
+            # C^T = R2 R1^T (masks: upper on the stored R factors); its QR gives
+            # the LQ preconditioner X = R_c^T of C (Jacobi converges in few sweeps)
+            gm_c.append((C, k2, Dim(k2, kR), Dim(k1, kL), 0.0,
+                         [(WR, n, 0, 1, WL, m, 1, 1, Dim(kcap, kL), 1.0)]))
+            qrc.append((C, tauC, tpC, None, k2, 0, Dim(k2, kR), Dim(k1, kL)))
+            svd.append((C, Uk, Xw, k2, k1, Dim(k1, kL), Dim(k2, kR), cap, p["rank_ri"],
+                        self.flag_slot, p["eps_slot"], p["eps_scale"], 1))
             U, ldu = p["U"]
             V, ldv = p["V"]
             apq.append((WL, tauL, tpL, U, Uk, m, ldu, k1, Dim(m), Dim(kcap, kL),
@@ -369,6 +373,7 @@ class Builder:
         self.ops.append(("concat", cat, dict(max_rows=maxrows)))
         self.ops.append(("qr", qr, {}))
         self.gemm(gm_c)
+        self.ops.append(("qr", qrc, {}))
         self.ops.append(("svd", svd, {}))
         self.ops.append(("applyq", apq, {}))
         self.gemm(gm_m)
@@ -449,6 +454,8 @@ class Builder:
         t = self.tree
         self.bumps[R_PHASE].reset()
         nl = t.size[v]
+        if nl > 512:
+            raise ValueError("leaf blocks larger than 512 are not supported by the leaf QR kernel")
         gat, qr = [], []
         for b in range(self.B):
             d = self.lay.m[b]
@@ -675,8 +682,9 @@ class CompiledPlan:
                 self.launch.append(("qr", put(pa), None, len(probs), extra))
             elif kind == "svd":
                 pa = np.zeros(len(probs), _abi.SVD_PROB)
-                for i, (c, u, ldc, ldu, m, n, cap, rri, fri, es, esc) in enumerate(probs):
-                    pa[i] = (A(c), A(u), ldc, ldu, m.cap, m.ri, n.cap, n.ri, cap, rri, fri, es, esc)
+                for i, (c, u, w, ldc, ldu, m, n, cap, rri, fri, es, esc, xf) in enumerate(probs):
+                    pa[i] = (A(c), A(u), A(w), ldc, ldu, m.cap, m.ri, n.cap, n.ri, cap, rri, fri, es,
+                             esc, xf, 0)
                 self.launch.append(("svd", put(pa), None, len(probs), extra))
             elif kind == "applyq":
                 pa = np.zeros(len(probs), _abi.APPLYQ_PROB)
@@ -788,7 +796,7 @@ def op_flops(kind, probs, rk):
             f += 4.0 * mm * r * cc - 2.0 * r * r * cc
     elif kind == "svd":
         for p in probs:
-            mm, nn = _dv(p[4], rk), _dv(p[5], rk)
+            mm, nn = _dv(p[5], rk), _dv(p[6], rk)
             a, b = max(mm, nn), min(mm, nn)
             f += 6.0 * a * b * b + 20.0 * b ** 3
     return f

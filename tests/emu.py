@@ -176,7 +176,12 @@ class Emu:
             if m <= 0 or n <= 0:
                 self.rank[p["rank_ri"]] = 0
                 continue
-            u, s, _ = np.linalg.svd(self.mat(p["c"], p["ldc"], m, n), full_matrices=False)
+            if p["xform"]:
+                n = min(n, m)
+                X = np.triu(self.mat(p["c"], p["ldc"], n, m)).T
+            else:
+                X = self.mat(p["c"], p["ldc"], m, n)
+            u, s, _ = np.linalg.svd(X, full_matrices=False)
             k = int(np.sum(s > thr))
             if k > p["cap"]:
                 if p["flag_ri"] >= 0:

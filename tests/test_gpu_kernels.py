@@ -100,8 +100,9 @@ def test_qr_and_applyq(dev, m, k):
     assert np.abs(back(dX, m, c) - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
 
 
-@pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60)])
-def test_svd_truncation(dev, m, n, keep):
+@pytest.mark.parametrize("xform", [0, 1])
+@pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60), (200, 190, 120)])
+def test_svd_truncation(dev, m, n, keep, xform):
     torch, lib = dev
     rng = np.random.default_rng(m * n)
     u = np.linalg.qr(rng.standard_normal((m, min(m, n))))[0]
@@ -109,12 +110,15 @@ def test_svd_truncation(dev, m, n, keep):
     s = np.logspace(0, -14, min(m, n))
     C = (u * s) @ v.T
     thr = float(s[keep]) * 1.000001 if keep < len(s) else 0.0
-    dC = colmajor(torch, C)
+    # xform=1 feeds R of C^T = Q R (the LQ preconditioner); X = R^T
+    dC = colmajor(torch, np.linalg.qr(C.T)[1] if xform else C)
+    ldc = min(m, n) if xform else m
+    dW = torch.zeros(m * n, dtype=torch.float64, device="cuda")
     dU = torch.zeros(m * min(m, n), dtype=torch.float64, device="cuda")
     rank = torch.zeros(4, dtype=torch.int32, device="cuda")
     scal = torch.zeros(2, dtype=torch.float64, device="cuda")
     p = np.zeros(1, _abi.SVD_PROB)
-    p[0] = (dC.data_ptr(), dU.data_ptr(), m, m, m, -1, n, -1, min(m, n), 0, 1, -1, thr)
+    p[0] = (dC.data_ptr(), dU.data_ptr(), dW.data_ptr(), ldc, m, m, -1, n, -1, min(m, n), 0, 1, -1, thr, xform, 0)
     dp = put(torch, p)
     assert lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr()) == 0
     torch.cuda.synchronize()

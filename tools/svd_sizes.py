@@ -13,7 +13,7 @@ rk = eng.h_rk_out.numpy()
 sizes = collections.Counter(); per_launch = []
 for kind, probs, extra in eng.builder.ops:
     if kind == "svd":
-        dims = [(_dv(p[4], rk), _dv(p[5], rk)) for p in probs]
+        dims = [(_dv(p[5], rk), _dv(p[6], rk)) for p in probs]
         per_launch.append((len(probs), max(m * n for m, n in dims), max(max(d) for d in dims)))
         for m, nn in dims:
             sizes[(min(m, nn) // 32 * 32)] += 1

@@ -1,0 +1,41 @@
+"""Per-launch device times (CUDA events, non-graph pass) with problem shapes."""
+import sys
+sys.path.insert(0, ".")
+import numpy as np, torch
+from paper_1809_10585_b200 import gen
+from paper_1809_10585_b200.hqr import HQREngine
+from paper_1809_10585_b200.plan import _dv
+ci = int(sys.argv[1]); n = int(sys.argv[2]) if len(sys.argv) > 2 else None
+top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+c = gen.CONFIGS[ci]
+a = gen.gen_config(ci, seed=0, n=n)
+eng = HQREngine(a.tree(), 1, c["tol"], use_graph=False)
+eng.factorize([a])
+rk = eng.h_rk_out.numpy()
+plan = eng.plan
+eng.upload(); torch.cuda.synchronize()
+s = eng.stream
+evs = []
+orig = plan.launch
+with torch.cuda.stream(s):
+    for rec in orig:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s); plan.launch = [rec]; plan.run(s.cuda_stream); e1.record(s)
+        evs.append((e0, e1))
+plan.launch = orig
+torch.cuda.synchronize()
+times = [e0.elapsed_time(e1) for e0, e1 in evs]
+ops = eng.builder.ops
+def shape(kind, probs):
+    if probs is None: return ""
+    if kind == "qr": return [( _dv(p[6], rk), _dv(p[7], rk), p[3] is not None) for p in probs][:4]
+    if kind == "svd": return [(_dv(p[5], rk), _dv(p[6], rk)) for p in probs][:4]
+    if kind == "applyq": return [(_dv(p[8], rk), _dv(p[9], rk), _dv(p[10], rk)) for p in probs][:4]
+    if kind == "gemm": return [(_dv(p[2], rk), _dv(p[3], rk), [_dv(t[8], rk) for t in p[5]][:3]) for p in probs][:3]
+    return len(probs)
+order = np.argsort(times)[::-1][:top]
+tot = sum(times)
+print(f"total {tot:.1f} ms over {len(times)} launches")
+for i in order:
+    kind, probs, ex = ops[i]
+    print(f"{times[i]:8.3f} ms  {kind:8s} nprob={0 if probs is None else len(probs):4d} {shape(kind, probs)}")
