@@ -164,7 +164,11 @@ int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_pie
               int* rank, int max_rows);
 int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank);
 int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank);
-int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal);
+/* cluster >= 2: one-sided block Jacobi on a cluster of `cluster` CTAs (2, 4
+   or 8) per problem, X distributed over their shared memories (DSMEM);
+   max_m bounds the row count (<= 512) and selects the lane-group width */
+int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal,
+           int cluster, int max_m);
 int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,
                    int* rank, int max_nl);
 int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,

@@ -61,7 +61,7 @@ SIGNATURES = {
     "hq_concat": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_qr": [_vp, _vp, _i, _vp],
     "hq_applyq": [_vp, _vp, _i, _vp],
-    "hq_svd": [_vp, _vp, _i, _vp, _vp],
+    "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i],
     "hq_leaf_gather": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_leaf_scatter": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_zero": [_vp, _vp, _i, _i64],

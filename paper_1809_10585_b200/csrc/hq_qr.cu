@@ -117,11 +117,17 @@ __device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, con
       const int a = mt * 8 + gq;          // A row  (reflector index)
       const int j = nt * 8 + gq;          // B col  (chunk column)
       const double* xc = X + (size_t)(c0 + j) * ldx;
-      for (int k0 = 0; k0 < rows; k0 += 4) {
-        const int ia = k0 + tq;           // A col / B row (matrix row)
-        const double av = (ia < rows && a < pw) ? yval(Y, ldy, ia, a) : 0.0;
-        const double bv = (ia < rows && j < cw) ? xc[ia] : 0.0;
-        dmma884(d0, d1, av, bv);
+      // loads for 8 k-steps issued back to back, then 8 DMMAs (latency hiding)
+      for (int k0 = 0; k0 < rows; k0 += 32) {
+        double av[8], bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int ia = k0 + 4 * u + tq;
+          av[u] = (ia < rows && a < pw) ? yval(Y, ldy, ia, a) : 0.0;
+          bv[u] = (ia < rows && j < cw) ? xc[ia] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
       }
       const int r = mt * 8 + gq, cc = nt * 8 + 2 * tq;
       S.wc[r + cc * NB] = d0;
@@ -191,9 +197,6 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
     // trailing columns: A_trail := Q_p^T A_trail
     if (p0 + pw < k)
       apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S);
-    if (staged) {
-      for (int e = t; e < rows * pw; e += NT) Pg[e % rows + (size_t)(e / rows) * ld] = P[e % rows + (e / rows) * ldp];
-    }
     __syncthreads();
     // full compact-WY T: T[0:p0, p] = -T[0:p0,0:p0] (Y[:,0:p0]^T Y_p) T_p   (wy.py:53)
     if (Q.tfull) {
@@ -208,11 +211,16 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
           const int mt = tile >> 1, nt = tile & 1;
           const int b = mt * 8 + gq, a = nt * 8 + gq;
           double d0 = 0.0, d1 = 0.0;
-          for (int k0 = 0; k0 < rows; k0 += 4) {
-            const int i = k0 + tq;
-            const double av = (i < rows && b < p0) ? W[(p0 + i) + (size_t)b * ld] : 0.0;
-            const double bv = (i < rows && a < pw) ? yval(Pg, ld, i, a) : 0.0;
-            dmma884(d0, d1, av, bv);
+          for (int k0 = 0; k0 < rows; k0 += 32) {
+            double av[8], bv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int i = k0 + 4 * u + tq;
+              av[u] = (i < rows && b < p0) ? W[(p0 + i) + (size_t)b * ld] : 0.0;
+              bv[u] = (i < rows && a < pw) ? yval(P, ldp, i, a) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
           }
           const int r = mt * 8 + gq, c = nt * 8 + 2 * tq;
           if (r < p0) { S.xs[r + c * MAXK_T] = d0; S.xs[r + (c + 1) * MAXK_T] = d1; }
@@ -238,11 +246,16 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
           const int mt = tile >> 1, nt = tile & 1;
           const int r = mt * 8 + gq, a = nt * 8 + gq;
           double d0 = 0.0, d1 = 0.0;
-          for (int k0 = (mt * 8) & ~3; k0 < p0; k0 += 4) {
-            const int c = k0 + tq;
-            const double av = (r < p0 && c < p0 && c >= r) ? -TF[r + (size_t)c * ldt] : 0.0;
-            const double bv = (c < p0 && a < pw) ? S.xs[c + a * MAXK_T] : 0.0;
-            dmma884(d0, d1, av, bv);
+          for (int k0 = mt * 8; k0 < p0; k0 += 32) {
+            double av[8], bv[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int c = k0 + 4 * u + tq;
+              av[u] = (r < p0 && c < p0 && c >= r) ? -TF[r + (size_t)c * ldt] : 0.0;
+              bv[u] = (c < p0 && a < pw) ? S.xs[c + a * MAXK_T] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
           }
           const int ro = mt * 8 + gq, co = nt * 8 + 2 * tq;
           if (ro < p0 && co < pw) TF[ro + (size_t)(p0 + co) * ldt] = d0;
@@ -251,6 +264,10 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
       }
       __syncthreads();
     }
+    if (staged) {
+      for (int e = t; e < rows * pw; e += NT) Pg[e % rows + (size_t)(e / rows) * ld] = P[e % rows + (e / rows) * ldp];
+    }
+    __syncthreads();
   }
 }
 

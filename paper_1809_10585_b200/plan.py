@@ -374,7 +374,7 @@ class Builder:
         self.ops.append(("qr", qr, {}))
         self.gemm(gm_c)
         self.ops.append(("qr", qrc, {}))
-        self.ops.append(("svd", svd, {}))
+        self.ops.append(("svd", svd, svd_cluster(svd)))
         self.ops.append(("applyq", apq, {}))
         self.gemm(gm_m)
         self.gemm(gm_v)
@@ -607,6 +607,24 @@ class Builder:
 
 # ---------------------------------------------------------------- packing
 
+SVD_SMEM_DOUBLES = 24576   # single-CTA staging capacity (hq_svd_kernel.cuh)
+CLUSTER_BUF_DOUBLES = 22528  # per-CTA block buffers (hq_svd_cluster.cuh)
+
+
+def svd_cluster(svd_probs):
+    """Pick single-CTA or cluster Jacobi for a launch from the capacities."""
+    mmax = max(p[5].cap for p in svd_probs)
+    nmax = max(min(p[5].cap, p[6].cap) for p in svd_probs)
+    ld = (mmax + 1) // 2 * 2
+    if ld * nmax <= SVD_SMEM_DOUBLES or mmax > 512:
+        return dict(cluster=1, max_m=mmax)
+    for g in (2, 4, 8):
+        bs = -(-nmax // (2 * g))
+        if 4 * bs * ld <= CLUSTER_BUF_DOUBLES and bs <= 64:
+            return dict(cluster=g, max_m=mmax)
+    return dict(cluster=1, max_m=mmax)
+
+
 def _addr(buf, bases, base_ptr):
     if buf is None:
         return 0
@@ -743,7 +761,7 @@ class CompiledPlan:
             elif kind == "qr":
                 rc = lib.hq_qr(stream_handle, dp + o1, cnt, rk)
             elif kind == "svd":
-                rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc)
+                rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0))
             elif kind == "applyq":
                 rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk)
             elif kind == "leaf_gather":

@@ -9,7 +9,10 @@ for n, kind in [(96, "decay"), (128, "decay"), (144, "decay"), (200, "decay"), (
     u = np.linalg.qr(rng.standard_normal((n, n)))[0]; v = np.linalg.qr(rng.standard_normal((n, n)))[0]
     s = {"decay": np.logspace(0, -14, n), "flat": np.ones(n), "lowrank": np.r_[np.logspace(0, -3, n // 2), np.zeros(n - n // 2)]}[kind]
     C = (u * s) @ v.T
-    for xf in (0, 1):
+    for xf, CL in ((1, 1), (1, 2), (1, 4), (1, 8)):
+        MM = n
+        ld, bs = (n + 1) // 2 * 2, -(-n // (2 * CL))
+        if CL > 1 and 4 * bs * ld > 22528: continue
         M = np.linalg.qr(C.T)[1] if xf else C
         for rep in range(2):
             dC = torch.tensor(M.T.copy(), device="cuda")
@@ -20,7 +23,7 @@ for n, kind in [(96, "decay"), (128, "decay"), (144, "decay"), (200, "decay"), (
             p = np.zeros(1, _abi.SVD_PROB); p[0] = (dC.data_ptr(), dU.data_ptr(), dW.data_ptr(), n, n, n, -1, n, -1, n, 0, 1, -1, 1e-10, xf, 0)
             dp = put(p); torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(); lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr()); e1.record(); torch.cuda.synchronize()
+            e0.record(); lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), CL, MM); e1.record(); torch.cuda.synchronize()
         k = int(rank[0]); U = dU.cpu().numpy().reshape(n, n).T[:, :k]
         err = np.linalg.norm(C - U @ (U.T @ C), 2)
-        print(n, kind, "xform", xf, "ms %.3f" % e0.elapsed_time(e1), "rank", k, "sweeps(dbg)", int(rank[2]), "proj err %.2e" % err, "orth %.1e" % np.abs(U.T @ U - np.eye(k)).max())
+        print(n, kind, "xform", xf, "cluster", CL, "ms %.3f" % e0.elapsed_time(e1), "rank", k, "sweeps(dbg)", int(rank[2]), "proj err %.2e" % err, "orth %.1e" % np.abs(U.T @ U - np.eye(k)).max())
