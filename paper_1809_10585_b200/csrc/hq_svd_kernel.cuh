@@ -30,12 +30,12 @@ __device__ __forceinline__ void pair_of(int r, int pi, int N, int& p, int& q) {
 // columns in registers (E = m / LP <= 16 doubles per lane per column): one
 // smem read and one smem write of each column per round, dot product reduced
 // with log2(LP) shuffles, the rotation parameters computed by the group.
-template <int LP, bool SMEM>
+template <int LP, bool SMEM, int E = 16>
 __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, double tiny2, double thr,
                              SvdSmem& S) {
   // SMEM: index the staged copy through S.cs so the compiler emits LDS/STS
   double* X = SMEM ? S.cs : Xg;
-  constexpr int E = 16, GPW = 32 / LP;
+  constexpr int GPW = 32 / LP;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int grp = wid * GPW + lane / LP, gl = lane % LP;
   const int ngroups = NW * GPW;
@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const hq_svd_prob* __restric
     // register-cached path: a group of LP lanes owns a pair (E <= 16 rows per lane)
     if (staged) {
       if (m <= 128) nsweeps = jacobi_groups<8, true>(X, ld, m, n, tol, tiny2, thr, S);
+      else if (m <= 192) nsweeps = jacobi_groups<8, true, 24>(X, ld, m, n, tol, tiny2, thr, S);
       else if (m <= 256) nsweeps = jacobi_groups<16, true>(X, ld, m, n, tol, tiny2, thr, S);
       else nsweeps = jacobi_groups<32, true>(X, ld, m, n, tol, tiny2, thr, S);
     } else {

@@ -185,6 +185,9 @@ class HQREngine(PlanIO):
         self.use_graph = use_graph
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.device)
+        self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
+        self.multi_stream = True
+        self._evs = []
 
     def upload(self):
         """H2D of the compact input stream, the rank table and the scalars."""
@@ -220,7 +223,25 @@ class HQREngine(PlanIO):
             self.d_px0 = self.d_px.clone()
 
     def _launch(self):
-        self.plan.run(self.stream.cuda_stream)
+        """Issue the plan: the critical chain on the engine stream, off-chain
+        work (R and T coupling blocks, non-spine recompressions) on side
+        streams, cross-stream dependencies as events -- a DAG once captured."""
+        torch = self.torch
+        if not self.side or not self.multi_stream:
+            self.plan.run(self.stream.cuda_stream)
+            return
+        self._evs = []
+
+        def mk():
+            e = torch.cuda.Event()
+            self._evs.append(e)
+            return e
+
+        fork = mk()
+        fork.record(self.stream)
+        for st in self.side:
+            st.wait_event(fork)
+        self.plan.run(self.stream.cuda_stream, [self.stream] + self.side, mk)
 
     def execute(self):
         """Run the factorization on the device (graph replay when captured)."""

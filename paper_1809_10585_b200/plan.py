@@ -38,8 +38,8 @@ NB = 16          # QR panel width (hq_qr.cu)
 GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
 SVD_MAX_N = 1024
 
-R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT = range(7)
-REGION_NAMES = ("persist", "phase", "apply", "trunc", "small", "in", "out")
+R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT, R_SHARED = range(8)
+LANE_STRIDE = 10   # scratch region of lane l: base + LANE_STRIDE * l (l = 0 main chain)
 
 
 class Buf:
@@ -63,18 +63,31 @@ class Dim:
 
 
 class Bump:
+    """Bump allocator of one region; remembers allocation starts so that any
+    address can be mapped back to the allocation that owns it."""
+
     def __init__(self, reg):
         self.reg, self.top, self.peak = reg, 0, 0
+        self.starts = set()
 
     def alloc(self, n):
         n = int(max(n, 1))
         b = Buf(self.reg, self.top)
+        self.starts.add(self.top)
         self.top += (n + 7) // 8 * 8
         self.peak = max(self.peak, self.top)
         return b
 
     def reset(self):
         self.top = 0
+
+    def finalize(self):
+        self.sorted = sorted(self.starts)
+
+    def owner(self, off):
+        import bisect
+        i = bisect.bisect_right(self.sorted, off) - 1
+        return self.sorted[max(i, 0)]
 
 
 class Tree:
@@ -183,12 +196,17 @@ class Builder:
     """Unrolls hqr_rec into batched ops with symbolic addresses."""
 
     def __init__(self, tree: PartitionTree, batch: int, eps: float, absolute: bool,
-                 kcap: int = 512, max_iter: int = 50, tol: float = 1e-3):
+                 kcap: int = 512, max_iter: int = 50, tol: float = 1e-3, n_side: int = 3):
         self.tree = Tree(tree)
         self.B = batch
         self.eps, self.absolute = float(eps), bool(absolute)
         self.max_iter, self.tol = max_iter, tol
-        self.bumps = [Bump(r) for r in range(7)]
+        self.bumps = {}
+        for r in range(8):
+            self.bump(r)
+        self.lane = 0
+        self.n_side = n_side
+        self._rr = 0
         self.slots = Slots()
         self.flag_slot = self.slots.take()
         self.power_done = self.slots.take(batch)
@@ -229,8 +247,35 @@ class Builder:
         return ins, outs
 
     # ------------------------------------------------------------ primitives
+    def bump(self, reg):
+        b = self.bumps.get(reg)
+        if b is None:
+            b = self.bumps[reg] = Bump(reg)
+        return b
+
+    def lane_bump(self, base):
+        return self.bump(base + LANE_STRIDE * self.lane)
+
     def _ph(self, n):
-        return self.bumps[R_PHASE].alloc(n)
+        return self.lane_bump(R_PHASE).alloc(n)
+
+    def _sh(self, n):
+        """Values read by several lanes: never reused (R_SHARED)."""
+        return self.bumps[R_SHARED].alloc(n)
+
+    def side_lane(self):
+        """Round-robin side lane for work off the critical chain; its scratch
+        regions are reset (the previous job of the lane precedes it in stream
+        order)."""
+        if self.n_side <= 0:
+            return 0
+        self._rr = self._rr % self.n_side + 1
+        return self._rr
+
+    def op(self, kind, probs, extra=None):
+        extra = dict(extra or {})
+        extra["lane"] = self.lane
+        self.ops.append((kind, probs, extra))
 
     def gemm(self, probs, skip=None, ksplit=1):
         """probs: list of (c, ldc, Dim m, Dim n, beta, [terms]); term =
@@ -240,11 +285,11 @@ class Builder:
         tiles = max(math.ceil(p[2].cap / GEMM_TILE) * math.ceil(p[3].cap / GEMM_TILE) for p in probs)
         if tiles <= 0:
             return
-        self.ops.append(("gemm", probs, dict(tiles=tiles, ksplit=ksplit, skip=skip)))
+        self.op("gemm", probs, dict(tiles=tiles, ksplit=ksplit, skip=skip))
 
     def zero(self, regions):
         if regions:
-            self.ops.append(("zero", regions, {}))
+            self.op("zero", regions)
 
     # ------------------------------------------------------------ HODLR x dense
     def _fset(self, fs, b):
@@ -267,7 +312,8 @@ class Builder:
         t = self.tree
         v0 = t.off[v]
         ncap, nris = nc
-        self.bumps[R_APPLY].reset()
+        ab = self.lane_bump(R_APPLY)
+        ab.reset()
         p1, p2, zeros, kmax = [], [], [], 0
         tmp = {}
         for b in range(self.B):
@@ -280,7 +326,7 @@ class Builder:
                 kc = self.lay.kc[u]
                 for kind, U, V, R in blocks:
                     rows0, nrows, cols0, ncols = (r1, m1, r2, m2) if kind == "a12" else (r2, m2, r1, m1)
-                    buf = self.bumps[R_APPLY].alloc(kc * ncap)
+                    buf = ab.alloc(kc * ncap)
                     tmp[(b, u, kind)] = buf
                     if trans:   # tmp = U^T X[rows]
                         term = (U[u], nrows, 1, 0, X + rows0, ldx, 0, 0, Dim(nrows), 1.0)
@@ -331,7 +377,7 @@ class Builder:
         eps_slot, eps_scale, U=(Buf, ld), V=(Buf, ld), cap, rank_ri)."""
         if not probs:
             return
-        z = self.bumps[R_TRUNC]
+        z = self.lane_bump(R_TRUNC)
         z.reset()
         cat, cat_pieces, qr, gm_c, qrc, svd, apq, gm_m, gm_v = [], [], [], [], [], [], [], [], []
         maxrows = 0
@@ -370,12 +416,12 @@ class Builder:
                          [(WL, m, 1, 1, Uk, k1, 0, 0, Dim(k1, kL), 1.0)]))
             gm_v.append((V, ldv, Dim(n), Dim(cap, p["rank_ri"]), 0.0,
                          [(WRc, n, 0, 0, Mm, kcap, 0, 0, Dim(kcap, kL), 1.0)]))
-        self.ops.append(("concat", cat, dict(max_rows=maxrows)))
-        self.ops.append(("qr", qr, {}))
+        self.op("concat", cat, dict(max_rows=maxrows))
+        self.op("qr", qr)
         self.gemm(gm_c)
-        self.ops.append(("qr", qrc, {}))
-        self.ops.append(("svd", svd, svd_cluster(svd)))
-        self.ops.append(("applyq", apq, {}))
+        self.op("qr", qrc)
+        self.op("svd", svd, svd_cluster(svd))
+        self.op("applyq", apq)
         self.gemm(gm_m)
         self.gemm(gm_v)
 
@@ -406,12 +452,12 @@ class Builder:
                  for b in range(self.B)]
             self.gemm(g, skip=skip)
             self.happly((0, 0), "A", True, ys, ws, (2, [-1] * self.B), skip=skip)
-            self.ops.append(("power", None, dict(n=n, final=int(it == self.max_iter - 1))))
+            self.op("power", None, dict(n=n, final=int(it == self.max_iter - 1)))
 
     def build(self):
         t = self.tree
         # restore the input from the compact staging buffer (first op)
-        self.ops.append(("pack_copy", self.in_items, dict(which=1, base=Buf(R_IN, 0), total=0)))
+        self.op("pack_copy", self.in_items, dict(which=1, base=Buf(R_IN, 0), total=0))
         if not self.absolute:
             self.power_iteration(t.n)
         # left-orthogonalize the a21 blocks of the leftmost spine: the only B
@@ -432,7 +478,9 @@ class Builder:
             self.trunc(probs)
         self.rec((0, 0))
         # compact the factors for one device->host copy (last op)
-        self.ops.append(("pack_copy", self.out_items, dict(which=0, base=Buf(R_OUT, 0), total=1)))
+        self.op("pack_copy", self.out_items, dict(which=0, base=Buf(R_OUT, 0), total=1))
+        for b in self.bumps.values():
+            b.finalize()
         return self
 
     def eps_slot(self, b):
@@ -452,7 +500,8 @@ class Builder:
     def leaf_qr(self, v):
         """Compressed leaf column -> block_qr (hqr.py:110-119)."""
         t = self.tree
-        self.bumps[R_PHASE].reset()
+        self.lane = 0
+        self.lane_bump(R_PHASE).reset()
         nl = t.size[v]
         if nl > 512:
             raise ValueError("leaf blocks larger than 512 are not supported by the leaf QR kernel")
@@ -468,15 +517,16 @@ class Builder:
             gat.append((d["leafA"][v], panel, nl, mcap, [(s[0], s[1], s[2], s[2], s[3]) for s in sl],
                         m_ri))
             qr.append((panel, tau, tp, d["leafT"][v], mcap, nl, Dim(mcap, m_ri), Dim(nl)))
-        self.ops.append(("leaf_gather", gat, dict(max_nl=nl)))
-        self.ops.append(("qr", qr, {}))
-        self.ops.append(("leaf_scatter", gat, dict(max_nl=nl)))
+        self.op("leaf_gather", gat, dict(max_nl=nl))
+        self.op("qr", qr)
+        self.op("leaf_scatter", gat, dict(max_nl=nl))
 
     def s_phase(self, v):
         """hqr.py:134-159: S~ (one recompression of the four-term sum), S, the
         R coupling block, and the update of the second block column."""
         t = self.tree
-        self.bumps[R_PHASE].reset()
+        self.lane = 0
+        self.lane_bump(R_PHASE).reset()
         c1, c2 = t.children(v)
         m1, m2 = t.size[c1], t.size[c2]
         kc = self.lay.kc[v]
@@ -491,7 +541,7 @@ class Builder:
         self.happly(c2, "A", True, [(D[b]["A21U"][v], m2) for b in B], [(tmp2[b], m2) for b in B],
                     (kc, [D[b]["rA21"][v] for b in B]))
         sL = [self._ph(m1 * cap_s) for _ in B]
-        sR = [self._ph(m2 * cap_s) for _ in B]
+        sR = [self._sh(m2 * cap_s) for _ in B]
         ks = [self.slots.take() for _ in B]
         probs = []
         for b in B:
@@ -505,9 +555,12 @@ class Builder:
                               U=(sL[b], m1), V=(sR[b], m2), cap=cap_s, rank_ri=ks[b]))
         self.trunc(probs)
         # S = T1^T S~ (hqr.py:150)
-        sL2 = [self._ph(m1 * cap_s) for _ in B]
+        sL2 = [self._sh(m1 * cap_s) for _ in B]
         self.happly(c1, "T", True, [(sL[b], m1) for b in B], [(sL2[b], m1) for b in B], (cap_s, ks))
-        # R's a12 = T([A12.L, -Y11 S.L], [A12.R; S.R]) (hqr.py:153-155)
+        # R's a12 = T([A12.L, -Y11 S.L], [A12.R; S.R]) (hqr.py:153-155): off the
+        # critical chain (only the output R reads it) -> side lane
+        self.lane = self.side_lane()
+        self.lane_bump(R_PHASE).reset()
         ys = [self._ph(m1 * cap_s) for _ in B]
         self.happly(c1, "Y", False, [(sL2[b], m1) for b in B], [(ys[b], m1) for b in B], (cap_s, ks))
         probs = []
@@ -519,9 +572,10 @@ class Builder:
                               eps_slot=self.eps_slot(b), eps_scale=1.0, U=(d["A12U"][v], m1),
                               V=(d["A12V"][v], m2), cap=kc, rank_ri=d["rA12"][v]))
         self.trunc(probs)
+        self.lane = 0
         # cross = QB (Y_B S.L) (hqr.py:156)
         w1 = [self._ph(kc * cap_s) for _ in B]
-        cross = [self._ph(m2 * cap_s) for _ in B]
+        cross = [self._sh(m2 * cap_s) for _ in B]
         ks1 = min(32, m1 // 256) if m1 >= 1024 else 1
         if ks1 > 1:
             self.zero([(w1[b], kc * cap_s) for b in B])
@@ -538,7 +592,15 @@ class Builder:
                 leafp.append((D[b]["leafA"][lf], nl, Dim(nl), Dim(nl), 1.0,
                               [(cross[b] + o, m2, 0, 0, sR[b] + o, m2, 1, 0, Dim(cap_s, ks[b]), -1.0)]))
         self.gemm(leafp)
-        probs = []
+        # the a21 blocks of c2's leftmost spine are the next B blocks of the
+        # chain: recompress them on the main lane, every other block of the
+        # subtree on a side lane (dependencies are tracked per buffer)
+        spine = set()
+        u = c2
+        while not t.is_leaf(u):
+            spine.add(u)
+            u = t.children(u)[0]
+        probs, side = [], []
         for b in B:
             d = D[b]
             for u in t.internal_nodes(c2) if not t.is_leaf(c2) else []:
@@ -550,12 +612,16 @@ class Builder:
                     else:
                         rs, rn, cs, cn, U, V, R = u2, t.size[u2], u1, t.size[u1], d["A21U"], d["A21V"], d["rA21"]
                     ro, co = t.off[rs] - t.off[c2], t.off[cs] - t.off[c2]
-                    probs.append(dict(m=rn, n=cn,
+                    (probs if (kind == "a21" and u in spine) else side).append(dict(m=rn, n=cn,
                                       L=[(U[u], rn, Dim(k_u, R[u]), 1.0), (cross[b] + ro, m2, Dim(cap_s, ks[b]), -1.0)],
                                       R=[(V[u], cn, Dim(k_u, R[u]), 1.0), (sR[b] + co, m2, Dim(cap_s, ks[b]), 1.0)],
                                       eps_slot=self.eps_slot(b), eps_scale=1.0, U=(U[u], rn), V=(V[u], cn),
                                       cap=k_u, rank_ri=R[u]))
         self.trunc(probs)
+        if side:
+            self.lane = self.side_lane()
+            self.trunc(side)
+            self.lane = 0
         # slab updates B_R2 -= (Y_B1 S.L) S.R, C2 likewise (hqr.py:158-159)
         zs, g1, g2, zero = [], [], [], []
         for b in B:
@@ -574,9 +640,11 @@ class Builder:
 
     def t_phase(self, v):
         """hqr.py:169-181: T~12 (one recompression of the three-term sum) and
-        T12 = -T1 T~12 T2."""
+        T12 = -T1 T~12 T2.  Runs on a side lane: only later S-phases (through
+        T(c1) of an ancestor) and the output read T12."""
         t = self.tree
-        self.bumps[R_PHASE].reset()
+        self.lane = self.side_lane()
+        self.lane_bump(R_PHASE).reset()
         c1, c2 = t.children(v)
         m1, m2 = t.size[c1], t.size[c2]
         kc = self.lay.kc[v]
@@ -603,6 +671,7 @@ class Builder:
                     (kc, rT), alpha=-1.0)
         self.happly(c2, "T", True, [(tR[b], m2) for b in B], [(D[b]["T12V"][v], m2) for b in B],
                     (kc, rT))
+        self.lane = 0
 
 
 # ---------------------------------------------------------------- packing
@@ -631,6 +700,127 @@ def _addr(buf, bases, base_ptr):
     return base_ptr + 8 * (bases[buf.reg] + buf.off)
 
 
+def op_resources(builder, kind, probs, extra):
+    """(reads, writes) of one op: allocations touched ('m', region, start),
+    rank-table slots ('r', slot) and the scalar table ('scal',).  The rank
+    capacity-overflow flag is excluded (it is only ever set)."""
+    R, W = set(), set()
+    bumps = builder.bumps
+
+    def mem(buf):
+        if buf is None:
+            return None
+        return ("m", buf.reg, bumps[buf.reg].owner(buf.off))
+
+    def rd(buf):
+        k = mem(buf)
+        if k:
+            R.add(k)
+
+    def wr(buf):
+        k = mem(buf)
+        if k:
+            W.add(k)
+
+    def slot(d, write=False):
+        ri = d.ri if isinstance(d, Dim) else d
+        if ri is not None and ri >= 0 and ri != builder.flag_slot:
+            (W if write else R).add(("r", ri))
+
+    if kind == "gemm":
+        if extra.get("skip") is not None:
+            slot(extra["skip"])
+        for (c, ldc, m, n, beta, terms) in probs:
+            wr(c)
+            if beta != 0.0 or extra.get("ksplit", 1) > 1:
+                rd(c)
+            slot(m), slot(n)
+            for t in terms:
+                rd(t[0]), rd(t[4]), slot(t[8])
+    elif kind == "zero":
+        for (buf, cnt) in probs:
+            wr(buf)
+    elif kind == "concat":
+        for (dst, dst2, rows, kri, pieces) in probs:
+            wr(dst), wr(dst2), slot(kri, True)
+            for (pp, ld, d, alpha) in pieces:
+                rd(pp), slot(d)
+    elif kind == "qr":
+        for (w, tau, tp, tf, ldw, ldt, m, k) in probs:
+            rd(w), wr(w), wr(tau), wr(tp), wr(tf), slot(m), slot(k)
+    elif kind == "svd":
+        for (c, u, w, ldc, ldu, m, n, cap, rri, fri, es, esc, xf) in probs:
+            rd(c), wr(c), wr(u), wr(w), slot(m), slot(n), slot(rri, True)
+            if es >= 0:
+                R.add(("scal",))
+    elif kind == "applyq":
+        for (w, tau, tp, x, x0, ldw, ldx, ldx0, m, k, c, r0, tr) in probs:
+            rd(w), rd(tau), rd(tp), rd(x0), rd(x), wr(x)
+            slot(m), slot(k), slot(c), slot(r0)
+    elif kind in ("leaf_gather", "leaf_scatter"):
+        for (leaf, panel, nl, ldp, slabs, mri) in probs:
+            if kind == "leaf_gather":
+                rd(leaf), wr(panel), slot(mri, True)
+                for (vv, yv, ld, ldy, kri) in slabs:
+                    rd(vv), slot(kri)
+            else:
+                rd(panel), wr(leaf), slot(mri)
+                for (vv, yv, ld, ldy, kri) in slabs:
+                    wr(yv), slot(kri)
+    elif kind == "power":
+        for buf in (builder.PX, builder.PW, builder.PG):
+            rd(buf)
+        wr(builder.PX)
+        R.add(("scal",)), W.add(("scal",))
+        for i in range(builder.B):
+            slot(builder.power_done + i), slot(builder.power_done + i, True)
+        for i in (0, 1):
+            slot(builder.all_done + i), slot(builder.all_done + i, True)
+    elif kind == "pack_copy":
+        if extra["which"] == 1:
+            rd(Buf(R_IN, 0))
+            for (buf, rows, cols) in probs:
+                wr(buf), slot(cols)
+        else:
+            W.add(("m", R_OUT, 0)), W.add(("totals",))
+            for (buf, rows, cols) in probs:
+                rd(buf), slot(cols)
+    else:
+        raise ValueError(kind)
+    return R, W
+
+
+def schedule(builder):
+    """Cross-lane dependencies of the op list (program order = a valid
+    topological order).  Returns lanes[i], waits[i] (ops of OTHER lanes op i
+    must wait for, latest per lane) and the set of ops that must signal."""
+    last_w, readers = {}, {}
+    lanes, waits, signal = [], [], set()
+    for i, (kind, probs, extra) in enumerate(builder.ops):
+        Rs, Ws = op_resources(builder, kind, probs, extra)
+        ln = extra.get("lane", 0)
+        deps = set()
+        for r in Rs | Ws:
+            if r in last_w:
+                deps.add(last_w[r])
+        for r in Ws:
+            deps.update(readers.get(r, ()))
+        per_lane = {}
+        for d in deps:
+            if lanes[d] != ln:
+                per_lane[lanes[d]] = max(per_lane.get(lanes[d], -1), d)
+        w = sorted(per_lane.values())
+        signal.update(w)
+        lanes.append(ln)
+        waits.append(w)
+        for r in Rs:
+            readers.setdefault(r, []).append(i)
+        for r in Ws:
+            last_w[r] = i
+            readers[r] = []
+    return lanes, waits, signal
+
+
 class CompiledPlan:
     """Ops packed into one device descriptor buffer; run() launches them."""
 
@@ -638,12 +828,12 @@ class CompiledPlan:
         import torch
         self.b = builder
         self.device = device
-        sizes = [bp.peak for bp in builder.bumps]
+        sizes = {r: bp.peak for r, bp in builder.bumps.items()}
         self.region_sizes = sizes
-        bases, acc = [], 0
-        for s in sizes:
-            bases.append(acc)
-            acc += (s + 63) // 64 * 64
+        bases, acc = {}, 0
+        for r in sorted(sizes):
+            bases[r] = acc
+            acc += (sizes[r] + 63) // 64 * 64
         self.total_doubles = acc
         self.arena = torch.zeros(max(acc, 1), dtype=torch.float64, device=device)
         self.rank = torch.zeros(max(builder.slots.n, 1), dtype=torch.int32, device=device)
@@ -739,18 +929,47 @@ class CompiledPlan:
             blob[start:start + len(raw)] = raw
         self.desc = torch.frombuffer(blob, dtype=torch.uint8).clone().to(device)
         self.n_launch = len(self.launch)
+        self.lanes, self.waits, self.signal = schedule(builder)
+        self.n_lanes = max(self.lanes) + 1 if self.lanes else 1
         self.graph = None
 
     def addr(self, buf):
         return _addr(buf, self.bases, self.arena.data_ptr())
 
-    def run(self, stream_handle: int):
+    def launch_one(self, lib, rec, stream_handle):
+        self._launch_list([rec], stream_handle, lib)
+
+    def run(self, stream_handle: int, streams=None, events=None):
+        """Launch every op.  With `streams` (torch streams indexed by lane)
+        and an event factory, ops go to their lane's stream and cross-lane
+        dependencies become event waits (DAG under graph capture)."""
         lib = _abi.load()
+        if streams is None or len(streams) == 1:
+            self._launch_list(self.launch, stream_handle, lib)
+            return
+        done = {}
+        for i, rec in enumerate(self.launch):
+            ln = self.lanes[i]
+            st = streams[ln]
+            for j in self.waits[i]:
+                st.wait_event(done[j])
+            self._launch_list([rec], st.cuda_stream, lib)
+            if i in self.signal:
+                ev = events()
+                ev.record(st)
+                done[i] = ev
+        # join every side stream back into the origin stream
+        for ln in range(1, len(streams)):
+            ev = events()
+            ev.record(streams[ln])
+            streams[0].wait_event(ev)
+
+    def _launch_list(self, launch, stream_handle, lib):
         dp = self.desc.data_ptr()
         rk = self.rank.data_ptr()
         sc = self.scal.data_ptr()
         b = self.b
-        for kind, o1, o2, cnt, ex in self.launch:
+        for kind, o1, o2, cnt, ex in launch:
             if kind == "gemm":
                 skip = rk + 4 * ex["skip"] if ex["skip"] is not None else None
                 rc = lib.hq_gemm(stream_handle, dp + o1, cnt, dp + o2, rk, ex["tiles"], ex["ksplit"], skip)

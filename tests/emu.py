@@ -259,8 +259,34 @@ class Emu:
             off += rows * cols
         self.plan.totals.numpy()[ex["total"]] = off
 
+    def run_interleaved(self, seed):
+        """Execute the ops in a random order that respects only the plan's
+        lanes (program order within a lane) and cross-lane waits -- what the
+        multi-stream graph guarantees.  A missed hazard changes the result."""
+        import random
+        rnd = random.Random(seed)
+        plan = self.plan
+        queues = {}
+        for i, ln in enumerate(plan.lanes):
+            queues.setdefault(ln, []).append(i)
+        pos = {ln: 0 for ln in queues}
+        done = set()
+        launch = plan.launch
+        while any(pos[ln] < len(q) for ln, q in queues.items()):
+            ready = [ln for ln, q in queues.items()
+                     if pos[ln] < len(q) and all(w in done for w in plan.waits[q[pos[ln]]])]
+            assert ready, "deadlock in the lane schedule"
+            ln = rnd.choice(ready)
+            i = queues[ln][pos[ln]]
+            pos[ln] += 1
+            self.run_ops([launch[i]])
+            done.add(i)
+
     def run(self):
-        for kind, o1, o2, cnt, ex in self.plan.launch:
+        self.run_ops(self.plan.launch)
+
+    def run_ops(self, ops):
+        for kind, o1, o2, cnt, ex in ops:
             if kind == "gemm":
                 self.gemm(o1, o2, cnt, ex)
             elif kind == "zero":
@@ -285,7 +311,7 @@ class Emu:
                 raise ValueError(kind)
 
 
-def emulate(mats, eps, absolute=False, kcap=512):
+def emulate(mats, eps, absolute=False, kcap=512, interleave_seed=None):
     """Run a plan for `mats` through the emulator; return (factors, io, plan)."""
     import torch
     from paper_1809_10585_b200.hqr import PlanIO
@@ -301,7 +327,10 @@ def emulate(mats, eps, absolute=False, kcap=512):
     A[pxo:pxo + io.px.size] = io.px
     plan.rank.numpy()[:] = io.rk
     plan.scal.numpy()[:] = io.sc
-    Emu(plan).run()
+    if interleave_seed is None:
+        Emu(plan).run()
+    else:
+        Emu(plan).run_interleaved(interleave_seed)
     rk = plan.rank.numpy().copy()
     if rk[io.builder.flag_slot]:
         raise RuntimeError("rank capacity overflow")

@@ -57,3 +57,16 @@ def test_rank_capacity_overflow_raises():
     a = gen.gen_random_hodlr(128, 32, 4, 8.0, seed=5)
     with pytest.raises(Exception):
         emulate([a], 1e-14, kcap=2)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_multistream_schedule_is_hazard_free(seed):
+    """Random interleavings allowed by the lane/event schedule give the same
+    factorization as program order (a missed dependency would not)."""
+    a = gen.gen_random_hodlr(256, 32, 4, 8.0, seed=0)
+    (f0,), _, _ = emulate([a], 1e-10)
+    (f1,), _, plan = emulate([a], 1e-10, interleave_seed=seed)
+    assert plan.n_lanes > 1
+    for k in ("y", "t", "r"):
+        d0, d1 = to_dense(getattr(f0, k)), to_dense(getattr(f1, k))
+        assert np.abs(d0 - d1).max() <= 1e-12 * max(1.0, np.abs(d0).max())
