@@ -186,7 +186,8 @@ class HQREngine(PlanIO):
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.device)
         self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
-        self.multi_stream = True
+        # side streams pay off when a launch leaves most SMs idle (few matrices)
+        self.multi_stream = batch <= 8
         self._evs = []
 
     def upload(self):
