@@ -162,8 +162,12 @@ int hq_gemm(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_te
             int* rank, int tiles, int ksplit, const int* skip);
 int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_piece* pieces,
               int* rank, int max_rows);
-int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank);
-int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank);
+/* cluster >= 2: each problem is factored by a cluster of 2/4/8 CTAs (column
+   blocks round-robin, panel factorization overlapped with the trailing
+   updates of the previous panel); requires tpanel != NULL */
+int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank, int cluster);
+/* grid = nprob x ceil(max_cols / 32): column chunks of X run on separate CTAs */
+int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank, int max_cols);
 /* cluster >= 2: one-sided block Jacobi on a cluster of `cluster` CTAs (2, 4
    or 8) per problem, X distributed over their shared memories (DSMEM);
    max_m bounds the row count (<= 512) and selects the lane-group width */

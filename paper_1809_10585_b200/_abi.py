@@ -59,8 +59,8 @@ SIGNATURES = {
     "hq_device_check": [],
     "hq_gemm": [_vp, _vp, _i, _vp, _vp, _i, _i, _vp],
     "hq_concat": [_vp, _vp, _i, _vp, _vp, _i],
-    "hq_qr": [_vp, _vp, _i, _vp],
-    "hq_applyq": [_vp, _vp, _i, _vp],
+    "hq_qr": [_vp, _vp, _i, _vp, _i],
+    "hq_applyq": [_vp, _vp, _i, _vp, _i],
     "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i],
     "hq_leaf_gather": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_leaf_scatter": [_vp, _vp, _i, _vp, _vp, _i],

@@ -7,6 +7,8 @@
 // One CTA per problem; panels of NB columns are staged in shared memory when
 // they fit, otherwise reduced in place in (L2-resident) global memory.
 #include "hq_common.cuh"
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 namespace {
 constexpr int NT = 256, NW = NT / 32, NB = 16;
@@ -17,7 +19,7 @@ constexpr int MAXK_T = 512;       // max columns when the full compact-WY T is f
 struct QrSmem {
   double panel[STAGE_ROWS * NB];
   double tp[NB * NB];
-  double d[NW][NB];
+  double dmat[NB * NB];   // dmat[c*NB + j] = y_c^T y_j (panel T recurrence)
   double dv[NB];
   double tcol[NB];
   double wc[NB * CW];
@@ -29,7 +31,75 @@ struct QrSmem {
 
 // Factor panel P (rows x pw, leading dim ldp; smem or global) into R + unit
 // lower reflectors, gammas into tau[0..pw), and its T factor into S.tp.
+// Column c of the panel is owned by warp c % NW: the owner forms reflector j
+// with warp-level reductions, one CTA barrier publishes it, then every warp
+// applies it to its own columns (dots with warp shuffles) and records the
+// y_c^T y_j products of the T recurrence (wy.py:37-39) -- one barrier per
+// column instead of a block-wide reduction per step.
 __device__ void panel_factor(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int j = 0; j < pw; ++j) {
+    if (wid == (j % NW)) {
+      double* cj = P + (size_t)j * ldp;
+      double ss = 0.0;
+      for (int i = j + 1 + lane; i < rows; i += 32) ss = fma(cj[i], cj[i], ss);
+      ss = warp_sum(ss);
+      const double x0 = cj[j];
+      const double nrm = sqrt(x0 * x0 + ss);
+      double gamma = 0.0, rho = 0.0, inv = 0.0;
+      if (nrm != 0.0) {
+        const double sg = x0 < 0.0 ? -1.0 : 1.0;   // sign(0) := +1
+        const double u1 = x0 + sg * nrm;           // no cancellation
+        rho = -sg * nrm;
+        inv = 1.0 / u1;
+        gamma = 2.0 / (1.0 + ss * inv * inv);
+      }
+      for (int i = j + 1 + lane; i < rows; i += 32) cj[i] *= inv;
+      __syncwarp();
+      if (lane == 0) {
+        cj[j] = rho;
+        S.dv[j] = gamma;
+        tau[j] = gamma;
+      }
+    }
+    __syncthreads();
+    const double gamma = S.dv[j];
+    const double* yj = P + (size_t)j * ldp;
+    for (int c = wid; c < pw; c += NW) {
+      if (c == j) continue;
+      double* cc = P + (size_t)c * ldp;
+      double d = 0.0;
+      for (int i = j + lane; i < rows; i += 32) d = fma(i == j ? 1.0 : yj[i], cc[i], d);
+      d = warp_sum(d);
+      if (c > j) {
+        const double gd = gamma * d;
+        for (int i = j + lane; i < rows; i += 32) cc[i] -= gd * (i == j ? 1.0 : yj[i]);
+      } else if (lane == 0) {
+        S.dmat[c * NB + j] = d;   // y_c^T y_j  (c < j)
+      }
+    }
+  }
+  __syncthreads();
+  // T (pw x pw): T[j][j] = gamma_j, T[0:j, j] = -gamma_j T[0:j,0:j] d[0:j, j]
+  if (wid == 0) {
+    for (int j = 0; j < pw; ++j) {
+      double v = 0.0;
+      if (lane < j) {
+        for (int a = lane; a < j; ++a) v = fma(S.tp[lane + a * NB], S.dmat[a * NB + j], v);
+      }
+      __syncwarp();
+      if (lane < j) S.tp[lane + j * NB] = -S.dv[j] * v;
+      if (lane == j) S.tp[j + j * NB] = S.dv[j];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// Block-wide variant for tall panels left in global memory: every warp
+// streams a slice of the rows (the warp-owned variant would serialize a tall
+// column on one warp).
+__device__ void panel_factor_block(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   for (int j = 0; j < pw; ++j) {
     double ss = 0.0;
@@ -68,12 +138,12 @@ __device__ void panel_factor(double* P, int ldp, int rows, int pw, double* tau, 
 #pragma unroll
     for (int c = 0; c < NB; ++c) {
       const double v = warp_sum(acc[c]);
-      if (lane == 0) S.d[wid][c] = v;
+      if (lane == 0) S.dmat[wid * NB + c] = v;
     }
     __syncthreads();
     if (t < NB) {
       double v = 0.0;
-      for (int w = 0; w < NW; ++w) v += S.d[w][t];
+      for (int w = 0; w < NW; ++w) v += S.dmat[w * NB + t];
       S.dv[t] = v;
     }
     __syncthreads();
@@ -103,8 +173,9 @@ __device__ __forceinline__ double yval(const double* P, int ldp, int i, int a) {
 // trans_t: T^T (applies Q^T) else T (applies Q).  Both products run on the
 // FP64 tensor pipe (mma.sync m8n8k4): W = Y^T X (16 x CW), W2 = T^op W,
 // X -= Y W2, column chunks of CW.
+template <class SM>
 __device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, const double* tp,
-                                 double* X, int ldx, int ncols, bool trans_t, QrSmem& S) {
+                                 double* X, int ldx, int ncols, bool trans_t, SM& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   for (int c0 = 0; c0 < ncols; c0 += CW) {
@@ -170,17 +241,14 @@ __device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, con
   }
 }
 
-__global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ probs,
-                                                int* __restrict__ rank) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  QrSmem& S = *reinterpret_cast<QrSmem*>(smem_raw);
-  const hq_qr_prob Q = probs[blockIdx.x];
-  const int m = hq_dim(rank, Q.m, Q.m_ri), k = hq_dim(rank, Q.k, Q.k_ri);
-  const int r = m < k ? m : k;
+// Factor panel p0 of problem Q: stage it (when it fits), reduce it, publish
+// gamma / T_p, (single-CTA path: update the trailing columns while the
+// panel is staged), merge T_p into the full compact-WY T when requested,
+// write the panel back.
+__device__ void factor_panel_step(const hq_qr_prob& Q, double* W, int ld, int m, int k, int r, int p0,
+                                  bool do_trailing, QrSmem& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  double* W = Q.w;
-  const int ld = Q.ldw;
-  for (int p0 = 0; p0 < r; p0 += NB) {
+  {
     const int pw = min(NB, r - p0), rows = m - p0;
     double* Pg = W + p0 + (size_t)p0 * ld;
     const bool staged = rows <= STAGE_ROWS;
@@ -192,10 +260,11 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
     }
     if (t < NB * NB) S.tp[t] = 0.0;
     __syncthreads();
-    panel_factor(P, ldp, rows, pw, Q.tau + p0, S);
+    if (staged) panel_factor(P, ldp, rows, pw, Q.tau + p0, S);
+    else panel_factor_block(P, ldp, rows, pw, Q.tau + p0, S);
     if (Q.tpanel && t < NB * NB) Q.tpanel[(size_t)(p0 / NB) * NB * NB + t] = S.tp[t];
     // trailing columns: A_trail := Q_p^T A_trail
-    if (p0 + pw < k)
+    if (do_trailing && p0 + pw < k)
       apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S);
     __syncthreads();
     // full compact-WY T: T[0:p0, p] = -T[0:p0,0:p0] (Y[:,0:p0]^T Y_p) T_p   (wy.py:53)
@@ -271,22 +340,99 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
   }
 }
 
-// X := Q X (trans = 0) or Q^T X (trans = 1), optionally X := [x0; 0] first.
-__global__ void __launch_bounds__(NT) applyq_kernel(const hq_applyq_prob* __restrict__ probs,
-                                                    int* __restrict__ rank) {
+__global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ probs,
+                                                int* __restrict__ rank) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrSmem& S = *reinterpret_cast<QrSmem*>(smem_raw);
-  const hq_applyq_prob A = probs[blockIdx.x];
-  const int m = hq_dim(rank, A.m, A.m_ri), k = hq_dim(rank, A.k, A.k_ri);
-  const int c = hq_dim(rank, A.c, A.c_ri);
+  const hq_qr_prob Q = probs[blockIdx.x];
+  const int m = hq_dim(rank, Q.m, Q.m_ri), k = hq_dim(rank, Q.k, Q.k_ri);
+  const int r = m < k ? m : k;
+  for (int p0 = 0; p0 < r; p0 += NB) factor_panel_step(Q, Q.w, Q.ldw, m, k, r, p0, true, S);
+}
+
+// Householder QR of one problem on a G-CTA cluster.  Column blocks of NB are
+// owned round-robin (block b by CTA b % G).  Phase ph: every CTA applies
+// panel ph-1 to its blocks >= ph -- the owner of block ph first, so that it
+// can factor panel ph immediately while the others are still updating -- and
+// one cluster barrier (release/acquire at cluster scope, covering the panel
+// and T_p written to global memory) separates the phases.
+template <int G>
+__global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __restrict__ probs,
+                                                           int* __restrict__ rank) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  QrSmem& S = *reinterpret_cast<QrSmem*>(smem_raw);
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  const hq_qr_prob Q = probs[blockIdx.x / G];
+  const int m = hq_dim(rank, Q.m, Q.m_ri), k = hq_dim(rank, Q.k, Q.k_ri);
   const int r = m < k ? m : k;
   const int t = threadIdx.x;
-  if (m <= 0 || c <= 0) return;
+  const int np = (r + NB - 1) / NB, nbk = (k + NB - 1) / NB;
+  double* W = Q.w;
+  const int ld = Q.ldw;
+  for (int ph = 0; ph <= np; ++ph) {
+    if (ph >= 1) {
+      const int q0 = (ph - 1) * NB, qw = min(NB, r - q0), rows = m - q0;
+      if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
+      __syncthreads();
+      const double* Y = W + q0 + (size_t)q0 * ld;
+      // a partial last panel (r not a multiple of NB, k > r): the rest of its
+      // own block lies beyond the reflectors and still needs panel ph-1
+      if (ph == np && qw < NB && k > r && ((ph - 1) % G) == cr) {
+        const int c1 = min(k, q0 + NB);
+        apply_panel_cols(Y, ld, rows, qw, S.tp, W + q0 + (size_t)r * ld, ld, c1 - r, true, S);
+      }
+      // my blocks b >= ph, block ph first
+      for (int pass = 0; pass < 2; ++pass) {
+        for (int b = ph; b < nbk; ++b) {
+          if (b % G != cr) continue;
+          const bool first = (b == ph);
+          if ((pass == 0) != first) continue;
+          const int c0 = b * NB, cw = min(NB, k - c0);
+          apply_panel_cols(Y, ld, rows, qw, S.tp, W + q0 + (size_t)c0 * ld, ld, cw, true, S);
+        }
+        if (pass == 0 && ph < np && (ph % G) == cr) {
+          factor_panel_step(Q, W, ld, m, k, r, ph * NB, false, S);
+          // factoring overwrote S.tp with T_ph: restore T_(ph-1) for pass 1
+          if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
+          __syncthreads();
+        }
+      }
+    } else if (np > 0 && cr == 0) {
+      factor_panel_step(Q, W, ld, m, k, r, 0, false, S);
+    }
+    __syncthreads();
+    cluster.sync();
+  }
+}
+
+struct ApqSmem {
+  double tp[NB * NB];
+  double wc[NB * CW];
+  double wc2[NB * CW];
+};
+
+// grid (problem, column chunk of APQ_CW): the columns of X are independent,
+// so each CTA applies all reflectors to its own chunk.
+constexpr int APQ_CW = 32;
+__global__ void __launch_bounds__(NT) applyq_kernel(const hq_applyq_prob* __restrict__ probs,
+                                                    int* __restrict__ rank) {
+  __shared__ ApqSmem S;
+  const hq_applyq_prob A = probs[blockIdx.x];
+  const int m = hq_dim(rank, A.m, A.m_ri), k = hq_dim(rank, A.k, A.k_ri);
+  const int call = hq_dim(rank, A.c, A.c_ri);
+  const int r = m < k ? m : k;
+  const int t = threadIdx.x;
+  const int cbeg = blockIdx.y * APQ_CW;
+  if (m <= 0 || cbeg >= call) return;
+  const int c = min(APQ_CW, call - cbeg);
+  double* X = A.x + (size_t)cbeg * A.ldx;
   if (A.x0) {
     const int r0 = hq_dim(rank, A.r0, A.r0_ri);
+    const double* X0 = A.x0 + (size_t)cbeg * A.ldx0;
     for (size_t e = t; e < (size_t)m * c; e += NT) {
       const int i = (int)(e % m), j = (int)(e / m);
-      A.x[i + (size_t)j * A.ldx] = i < r0 ? A.x0[i + (size_t)j * A.ldx0] : 0.0;
+      X[i + (size_t)j * A.ldx] = i < r0 ? X0[i + (size_t)j * A.ldx0] : 0.0;
     }
     __syncthreads();
   }
@@ -296,7 +442,7 @@ __global__ void __launch_bounds__(NT) applyq_kernel(const hq_applyq_prob* __rest
     const int p0 = p * NB, pw = min(NB, r - p0), rows = m - p0;
     if (t < NB * NB) S.tp[t] = A.tpanel[(size_t)p * NB * NB + t];
     __syncthreads();
-    apply_panel_cols(A.w + p0 + (size_t)p0 * A.ldw, A.ldw, rows, pw, S.tp, A.x + p0, A.ldx, c,
+    apply_panel_cols(A.w + p0 + (size_t)p0 * A.ldw, A.ldw, rows, pw, S.tp, X + p0, A.ldx, c,
                      A.trans != 0, S);
   }
 }
@@ -424,26 +570,52 @@ static int qr_smem_attr() {
   if (!g_attr_done) {
     cudaError_t e = cudaFuncSetAttribute(qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QrSmem));
     if (e != cudaSuccess) return (int)e;
-    e = cudaFuncSetAttribute(applyq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QrSmem));
-    if (e != cudaSuccess) return (int)e;
     g_attr_done = true;
   }
   return 0;
 }
 
-extern "C" int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank) {
+template <int G>
+static int launch_qr_cluster(cudaStream_t st, const hq_qr_prob* probs, int nprob, int* rank) {
+  static bool attr = false;
+  auto kern = qr_cluster_kernel<G>;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QrSmem));
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nprob * G);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = sizeof(QrSmem);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, kern, probs, rank);
+}
+
+extern "C" int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank, int cluster) {
   if (nprob <= 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cluster >= 8) return launch_qr_cluster<8>(st, probs, nprob, rank);
+  if (cluster >= 4) return launch_qr_cluster<4>(st, probs, nprob, rank);
+  if (cluster >= 2) return launch_qr_cluster<2>(st, probs, nprob, rank);
   int e = qr_smem_attr();
   if (e) return e;
-  qr_kernel<<<nprob, NT, sizeof(QrSmem), (cudaStream_t)stream>>>(probs, rank);
+  qr_kernel<<<nprob, NT, sizeof(QrSmem), st>>>(probs, rank);
   return hq_err(cudaGetLastError());
 }
 
-extern "C" int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank) {
+extern "C" int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank,
+                         int max_cols) {
   if (nprob <= 0) return 0;
-  int e = qr_smem_attr();
-  if (e) return e;
-  applyq_kernel<<<nprob, NT, sizeof(QrSmem), (cudaStream_t)stream>>>(probs, rank);
+  const int nchunk = max_cols > 0 ? (max_cols + APQ_CW - 1) / APQ_CW : 1;
+  applyq_kernel<<<dim3(nprob, nchunk), NT, 0, (cudaStream_t)stream>>>(probs, rank);
   return hq_err(cudaGetLastError());
 }
 

@@ -275,6 +275,8 @@ class Builder:
     def op(self, kind, probs, extra=None):
         extra = dict(extra or {})
         extra["lane"] = self.lane
+        if kind == "qr" and "cluster" not in extra:
+            extra["cluster"] = qr_cluster(probs)
         self.ops.append((kind, probs, extra))
 
     def gemm(self, probs, skip=None, ksplit=1):
@@ -421,7 +423,7 @@ class Builder:
         self.gemm(gm_c)
         self.op("qr", qrc)
         self.op("svd", svd, svd_cluster(svd))
-        self.op("applyq", apq)
+        self.op("applyq", apq, dict(max_cols=max(p[10].cap for p in apq)))
         self.gemm(gm_m)
         self.gemm(gm_v)
 
@@ -450,7 +452,10 @@ class Builder:
             g = [(self.PG + 4 * b, 2, Dim(2), Dim(2), 0.0,
                   [(self.PY + 2 * n * b, n, 1, 0, self.PY + 2 * n * b, n, 0, 0, Dim(n), 1.0)])
                  for b in range(self.B)]
-            self.gemm(g, skip=skip)
+            gs = min(64, max(1, n // 256))
+            if gs > 1:
+                self.zero([(self.PG + 4 * b, 4) for b in range(self.B)])
+            self.gemm(g, skip=skip, ksplit=gs)
             self.happly((0, 0), "A", True, ys, ws, (2, [-1] * self.B), skip=skip)
             self.op("power", None, dict(n=n, final=int(it == self.max_iter - 1)))
 
@@ -678,6 +683,18 @@ class Builder:
 
 SVD_SMEM_DOUBLES = 24576   # single-CTA staging capacity (hq_svd_kernel.cuh)
 CLUSTER_BUF_DOUBLES = 22528  # per-CTA block buffers (hq_svd_cluster.cuh)
+
+
+def qr_cluster(qr_probs):
+    """Cluster size for a QR launch: spread few, wide problems over several
+    SMs; many problems (or narrow ones) run one CTA each."""
+    n = len(qr_probs)
+    kmax = max(p[7].cap for p in qr_probs)
+    if kmax < 48 or n > 74:
+        return 1
+    if n <= 18:
+        return 8
+    return 4 if n <= 37 else 2
 
 
 def svd_cluster(svd_probs):
@@ -978,11 +995,11 @@ class CompiledPlan:
             elif kind == "concat":
                 rc = lib.hq_concat(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_rows"])
             elif kind == "qr":
-                rc = lib.hq_qr(stream_handle, dp + o1, cnt, rk)
+                rc = lib.hq_qr(stream_handle, dp + o1, cnt, rk, ex.get("cluster", 1))
             elif kind == "svd":
                 rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0))
             elif kind == "applyq":
-                rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk)
+                rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk, ex.get("max_cols", 0))
             elif kind == "leaf_gather":
                 rc = lib.hq_leaf_gather(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
             elif kind == "leaf_scatter":

@@ -54,8 +54,10 @@ def test_gemm(dev, m, n, k, ta, tb):
     assert np.allclose(back(dC, m, n), ref, atol=1e-12 * max(1, np.abs(ref).max()))
 
 
-@pytest.mark.parametrize("m,k", [(25, 25), (28, 25), (9, 6), (300, 40), (50, 70), (1200, 17), (200, 200), (60, 57)])
-def test_qr_and_applyq(dev, m, k):
+@pytest.mark.parametrize("cl", [1, 2, 8])
+@pytest.mark.parametrize("m,k", [(25, 25), (28, 25), (9, 6), (300, 40), (50, 70), (1200, 17), (200, 200), (60, 57),
+                                 (352, 256)])
+def test_qr_and_applyq(dev, m, k, cl):
     torch, lib = dev
     rng = np.random.default_rng(m + 7 * k)
     A = rng.standard_normal((m, k))
@@ -69,7 +71,7 @@ def test_qr_and_applyq(dev, m, k):
     q = np.zeros(1, _abi.QR_PROB)
     q[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), tf.data_ptr(), m, r, m, -1, k, -1)
     dq = put(torch, q)
-    assert lib.hq_qr(None, dq.data_ptr(), 1, rank.data_ptr()) == 0
+    assert lib.hq_qr(None, dq.data_ptr(), 1, rank.data_ptr(), cl) == 0
     torch.cuda.synchronize()
     W = back(dW, m, k)
     R = np.triu(W[:r])
@@ -94,7 +96,7 @@ def test_qr_and_applyq(dev, m, k):
     ap[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), dX.data_ptr(), dX0.data_ptr(), m, m, r,
              m, -1, k, -1, c, -1, r, -1, 0)
     da = put(torch, ap)
-    assert lib.hq_applyq(None, da.data_ptr(), 1, rank.data_ptr()) == 0
+    assert lib.hq_applyq(None, da.data_ptr(), 1, rank.data_ptr(), c) == 0
     torch.cuda.synchronize()
     ref = Q[:, :r] @ X0
     assert np.abs(back(dX, m, c) - ref).max() <= 1e-12 * max(1, np.abs(ref).max())

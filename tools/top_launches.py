@@ -39,3 +39,20 @@ print(f"total {tot:.1f} ms over {len(times)} launches")
 for i in order:
     kind, probs, ex = ops[i]
     print(f"{times[i]:8.3f} ms  {kind:8s} nprob={0 if probs is None else len(probs):4d} {shape(kind, probs)}")
+# breakdown by kind / size class
+import collections
+agg = collections.defaultdict(lambda: [0.0, 0])
+for i, (kind, probs, ex) in enumerate(ops):
+    key = kind
+    if kind == "qr" and probs:
+        mm = max(_dv(p[6], rk) for p in probs)
+        leaf = probs[0][3] is not None
+        key = f"qr {'leaf' if leaf else 'trunc'} m{'<=512' if mm <= 512 else ('<=1024' if mm <= 1024 else '>1024')}"
+    elif kind == "svd" and probs:
+        key = f"svd cl{ex.get('cluster',1)}"
+    elif kind == "gemm" and probs:
+        kk = max(max((_dv(t[8], rk) for t in p[5]), default=0) for p in probs)
+        key = f"gemm k{'<=256' if kk <= 256 else ('<=2048' if kk <= 2048 else '>2048')} split{ex['ksplit']}"
+    agg[key][0] += times[i]; agg[key][1] += 1
+for k, (tm, c) in sorted(agg.items(), key=lambda x: -x[1][0]):
+    print(f"{k:32s} {c:5d} launches {tm:9.1f} ms")
