@@ -545,20 +545,44 @@ class Builder:
                     (kc, [D[b]["rA12"][v] for b in B]))
         self.happly(c2, "A", True, [(D[b]["A21U"][v], m2) for b in B], [(tmp2[b], m2) for b in B],
                     (kc, [D[b]["rA21"][v] for b in B]))
-        sL = [self._ph(m1 * cap_s) for _ in B]
-        sR = [self._sh(m2 * cap_s) for _ in B]
-        ks = [self.slots.take() for _ in B]
-        probs = []
+        # S~ = T(T(T(t1 + t2) + t3) + t4): the left-to-right sum of hqr.py:143-147,
+        # truncating after every addition exactly like the reference (for
+        # ill-conditioned A the computed R is sensitive to this sequence)
+        own = [[], []]
+        rest = [[], []]
         for b in B:
-            d = D[b]
-            Lp = [(tmp1[b], m1, Dim(kc, d["rA12"][v]), 1.0), (d["YV21"][v], m1, Dim(kc, d["rA21"][v]), 1.0)]
-            Rp = [(d["A12V"][v], m2, Dim(kc, d["rA12"][v]), 1.0), (tmp2[b], m2, Dim(kc, d["rA21"][v]), 1.0)]
-            for (vc1, yc1, ld, ri, kw), (vc2, yc2, _, _, _) in zip(self.slabs(b, v, c1), self.slabs(b, v, c2)):
-                Lp.append((yc1, ld, Dim(kw, ri), 1.0))
-                Rp.append((vc2, ld, Dim(kw, ri), 1.0))
-            probs.append(dict(m=m1, n=m2, L=Lp, R=Rp, eps_slot=self.eps_slot(b), eps_scale=1.0,
-                              U=(sL[b], m1), V=(sR[b], m2), cap=cap_s, rank_ri=ks[b]))
-        self.trunc(probs)
+            sl1, sl2 = self.slabs(b, v, c1), self.slabs(b, v, c2)
+            first = v[0] > 0 and v[1] % 2 == 0
+            own[0].append(sl1[:1] if first else [])
+            own[1].append(sl2[:1] if first else [])
+            rest[0].append(sl1[1:] if first else sl1)
+            rest[1].append(sl2[1:] if first else sl2)
+        cur_L = [[(tmp1[b], m1, Dim(kc, D[b]["rA12"][v]), 1.0)] for b in B]
+        cur_R = [[(D[b]["A12V"][v], m2, Dim(kc, D[b]["rA12"][v]), 1.0)] for b in B]
+        adds = [
+            ([[(D[b]["YV21"][v], m1, Dim(kc, D[b]["rA21"][v]), 1.0)] for b in B],
+             [[(tmp2[b], m2, Dim(kc, D[b]["rA21"][v]), 1.0)] for b in B]),
+            ([[(yc1, ld, Dim(kw, ri), 1.0) for (vc1, yc1, ld, ri, kw) in own[0][b]] for b in B],
+             [[(vc2, ld, Dim(kw, ri), 1.0) for (vc2, yc2, ld, ri, kw) in own[1][b]] for b in B]),
+            ([[(yc1, ld, Dim(kw, ri), 1.0) for (vc1, yc1, ld, ri, kw) in rest[0][b]] for b in B],
+             [[(vc2, ld, Dim(kw, ri), 1.0) for (vc2, yc2, ld, ri, kw) in rest[1][b]] for b in B]),
+        ]
+        for step, (addL, addR) in enumerate(adds):
+            last = step == len(adds) - 1
+            outL = [self._ph(m1 * cap_s) for _ in B]
+            outR = [(self._sh if last else self._ph)(m2 * cap_s) for _ in B]
+            kk = [self.slots.take() for _ in B]
+            probs = []
+            for b in B:
+                probs.append(dict(m=m1, n=m2, L=cur_L[b] + addL[b], R=cur_R[b] + addR[b],
+                                  eps_slot=self.eps_slot(b), eps_scale=1.0,
+                                  U=(outL[b], m1), V=(outR[b], m2), cap=cap_s, rank_ri=kk[b]))
+            self.trunc(probs)
+            cur_L = [[(outL[b], m1, Dim(cap_s, kk[b]), 1.0)] for b in B]
+            cur_R = [[(outR[b], m2, Dim(cap_s, kk[b]), 1.0)] for b in B]
+        sL = [cur_L[b][0][0] for b in B]
+        sR = [cur_R[b][0][0] for b in B]
+        ks = kk
         # S = T1^T S~ (hqr.py:150)
         sL2 = [self._sh(m1 * cap_s) for _ in B]
         self.happly(c1, "T", True, [(sL[b], m1) for b in B], [(sL2[b], m1) for b in B], (cap_s, ks))
@@ -658,19 +682,32 @@ class Builder:
         tmp3 = [self._ph(m2 * kc) for _ in B]
         self.happly(c2, "Y", True, [(D[b]["A21U"][v], m2) for b in B], [(tmp3[b], m2) for b in B],
                     (kc, [D[b]["rA21"][v] for b in B]))
-        tL = [self._ph(m1 * kc) for _ in B]
-        tR = [self._ph(m2 * kc) for _ in B]
-        probs = []
-        for b in B:
-            d = D[b]
-            Lp = [(d["YV21"][v], m1, Dim(kc, d["rA21"][v]), 1.0)]
-            Rp = [(tmp3[b], m2, Dim(kc, d["rA21"][v]), 1.0)]
-            for (vc1, yc1, ld, ri, kw), (vc2, yc2, _, _, _) in zip(self.slabs(b, v, c1), self.slabs(b, v, c2)):
-                Lp.append((yc1, ld, Dim(kw, ri), 1.0))
-                Rp.append((yc2, ld, Dim(kw, ri), 1.0))
-            probs.append(dict(m=m1, n=m2, L=Lp, R=Rp, eps_slot=-1, eps_scale=self.eps,
-                              U=(tL[b], m1), V=(tR[b], m2), cap=kc, rank_ri=d["rT12"][v]))
-        self.trunc(probs)
+        # T~12 = T(T(u1 + u2) + u3) with the plain eps (hqr.py:170-179)
+        first = v[0] > 0 and v[1] % 2 == 0
+        cur_L = [[(D[b]["YV21"][v], m1, Dim(kc, D[b]["rA21"][v]), 1.0)] for b in B]
+        cur_R = [[(tmp3[b], m2, Dim(kc, D[b]["rA21"][v]), 1.0)] for b in B]
+        sl = [(self.slabs(b, v, c1), self.slabs(b, v, c2)) for b in B]
+        adds = [
+            ([[(y1, ld, Dim(kw, ri), 1.0) for (v1, y1, ld, ri, kw) in (sl[b][0][:1] if first else [])] for b in B],
+             [[(y2, ld, Dim(kw, ri), 1.0) for (v2, y2, ld, ri, kw) in (sl[b][1][:1] if first else [])] for b in B]),
+            ([[(y1, ld, Dim(kw, ri), 1.0) for (v1, y1, ld, ri, kw) in (sl[b][0][1:] if first else sl[b][0])] for b in B],
+             [[(y2, ld, Dim(kw, ri), 1.0) for (v2, y2, ld, ri, kw) in (sl[b][1][1:] if first else sl[b][1])] for b in B]),
+        ]
+        for step, (addL, addR) in enumerate(adds):
+            last = step == len(adds) - 1
+            outL = [self._ph(m1 * kc) for _ in B]
+            outR = [self._ph(m2 * kc) for _ in B]
+            kk = [D[b]["rT12"][v] if last else self.slots.take() for b in B]
+            probs = []
+            for b in B:
+                probs.append(dict(m=m1, n=m2, L=cur_L[b] + addL[b], R=cur_R[b] + addR[b], eps_slot=-1,
+                                  eps_scale=self.eps, U=(outL[b], m1), V=(outR[b], m2), cap=kc,
+                                  rank_ri=kk[b]))
+            self.trunc(probs)
+            cur_L = [[(outL[b], m1, Dim(kc, kk[b]), 1.0)] for b in B]
+            cur_R = [[(outR[b], m2, Dim(kc, kk[b]), 1.0)] for b in B]
+        tL = [cur_L[b][0][0] for b in B]
+        tR = [cur_R[b][0][0] for b in B]
         rT = [D[b]["rT12"][v] for b in B]
         self.happly(c1, "T", False, [(tL[b], m1) for b in B], [(D[b]["T12U"][v], m1) for b in B],
                     (kc, rT), alpha=-1.0)
