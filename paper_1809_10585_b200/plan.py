@@ -567,6 +567,9 @@ class Builder:
             ([[(yc1, ld, Dim(kw, ri), 1.0) for (vc1, yc1, ld, ri, kw) in rest[0][b]] for b in B],
              [[(vc2, ld, Dim(kw, ri), 1.0) for (vc2, yc2, ld, ri, kw) in rest[1][b]] for b in B]),
         ]
+        # a statically empty term (no B block, no ancestor slabs) makes the
+        # reference re-truncate an already truncated sum: T(T(x)) = T(x), skip
+        adds = [ad for i, ad in enumerate(adds) if i == 0 or any(ad[0][b] for b in B)]
         for step, (addL, addR) in enumerate(adds):
             last = step == len(adds) - 1
             outL = [self._ph(m1 * cap_s) for _ in B]
@@ -693,6 +696,9 @@ class Builder:
             ([[(y1, ld, Dim(kw, ri), 1.0) for (v1, y1, ld, ri, kw) in (sl[b][0][1:] if first else sl[b][0])] for b in B],
              [[(y2, ld, Dim(kw, ri), 1.0) for (v2, y2, ld, ri, kw) in (sl[b][1][1:] if first else sl[b][1])] for b in B]),
         ]
+        # T(u1 + 0) is still a truncation of the untruncated u1 (kept); an
+        # empty last term would only re-truncate (skipped, T(T(x)) = T(x))
+        adds = [ad for i, ad in enumerate(adds) if i == 0 or any(ad[0][b] for b in B)]
         for step, (addL, addR) in enumerate(adds):
             last = step == len(adds) - 1
             outL = [self._ph(m1 * kc) for _ in B]
