@@ -21,6 +21,18 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const hq_gemm_prob* __restrict
   const int tile = blockIdx.x;
   if (tile >= ntm * ntn) return;
   const int i0 = (tile % ntm) * BM, j0 = (tile / ntm) * BN;
+  // per-problem split: at least 8 k-tiles per slice (short-K problems of a
+  // split launch keep one slice; the output was pre-zeroed either way)
+  int ks = ksplit;
+  if (ksplit > 1) {
+    int nkt = 0;
+    for (int ti = 0; ti < P.nterm; ++ti) {
+      const hq_gemm_term T = terms[P.term0 + ti];
+      nkt += (hq_dim(rank, T.k, T.k_ri) + BK - 1) / BK;
+    }
+    ks = min(ksplit, max(1, nkt / 8));
+    if ((int)blockIdx.z >= ks) return;
+  }
 
   __shared__ double As[BK][BM + 1];
   __shared__ double Bs[BK][BN + 1];
@@ -36,7 +48,7 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const hq_gemm_prob* __restrict
     const hq_gemm_term T = terms[P.term0 + ti];
     const int kd = hq_dim(rank, T.k, T.k_ri);
     for (int k0 = 0; k0 < kd; k0 += BK, ++gk) {
-      if (ksplit > 1 && (gk % ksplit) != (int)blockIdx.z) continue;
+      if (ks > 1 && (gk % ks) != (int)blockIdx.z) continue;
       // ---- A tile: op(A)(i, kk)
 #pragma unroll
       for (int r = 0; r < 4; ++r) {

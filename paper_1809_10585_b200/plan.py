@@ -340,7 +340,7 @@ class Builder:
                     zeros.append((buf, kc * ncap))
         ksplit = 1
         if kmax >= 1024:
-            ksplit = min(32, kmax // 256)
+            ksplit = min(32, kmax // 256)   # per problem the kernel uses <= nktiles/8 slices
         if p1:
             if ksplit > 1:
                 self.zero(zeros)
@@ -741,8 +741,11 @@ def qr_cluster(qr_probs):
 
 
 def svd_cluster(svd_probs):
-    """Pick single-CTA or cluster Jacobi for a launch from the capacities."""
+    """Pick single-CTA or cluster Jacobi for a launch from the capacities;
+    launches with many problems already fill the GPU one CTA each."""
     mmax = max(p[5].cap for p in svd_probs)
+    if len(svd_probs) > 18:
+        return dict(cluster=1, max_m=mmax)
     nmax = max(min(p[5].cap, p[6].cap) for p in svd_probs)
     ld = (mmax + 1) // 2 * 2
     if ld * nmax <= SVD_SMEM_DOUBLES or mmax > 512:

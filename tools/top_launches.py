@@ -5,12 +5,14 @@ import numpy as np, torch
 from paper_1809_10585_b200 import gen
 from paper_1809_10585_b200.hqr import HQREngine
 from paper_1809_10585_b200.plan import _dv
-ci = int(sys.argv[1]); n = int(sys.argv[2]) if len(sys.argv) > 2 else None
+ci = int(sys.argv[1]); n = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "0" else None
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+B = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 c = gen.CONFIGS[ci]
-a = gen.gen_config(ci, seed=0, n=n)
-eng = HQREngine(a.tree(), 1, c["tol"], use_graph=False)
-eng.factorize([a])
+mats = [gen.gen_config(ci, seed=s, n=n) for s in range(B)]
+a = mats[0]
+eng = HQREngine(a.tree(), B, c["tol"], use_graph=False)
+eng.factorize(mats)
 rk = eng.h_rk_out.numpy()
 plan = eng.plan
 eng.upload(); torch.cuda.synchronize()
