@@ -58,7 +58,12 @@ def test_full_config_vs_reference(ci):
     G = np.random.default_rng(0x5C37).standard_normal((a.n, 8))
     rg = O.happly(f.r, G)
     rel = np.linalg.norm(rg - g["RG"]) / np.linalg.norm(g["RG"])
-    assert rel <= 100 * c["tol"], rel
+    # north star: R within 100*tol of the reference's R.  Where the reference
+    # itself is not reproducible to that level (config 2, kappa ~1e17: its
+    # numpy restatement differs by r_sketch_floor, tests/golden/oracle_floor.py)
+    # the GPU must stay within 10x that rounding floor.
+    bound = max(100 * c["tol"], 10 * float(g.get("r_sketch_floor", 0.0)))
+    assert rel <= bound, (rel, bound)
     e_orth, e_acc = estimate_metrics(a, f)
     assert e_orth <= 10 * max(float(g["e_orth"]), 1e-14), (e_orth, float(g["e_orth"]))
     assert e_acc <= 10 * max(float(g["e_acc"]), 1e-14 * float(g["norm_est"])), (e_acc, float(g["e_acc"]))
