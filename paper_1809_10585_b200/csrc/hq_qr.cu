@@ -10,11 +10,18 @@
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
+#ifdef HQ_DEBUG_TIMING
+__device__ long long* hq_dbg = nullptr;
+extern "C" int hq_debug_set(void* p) {
+  return (int)cudaMemcpyToSymbol(hq_dbg, &p, sizeof(p));
+}
+#endif
 namespace {
 constexpr int NT = 256, NW = NT / 32, NB = 16;
 constexpr int STAGE_ROWS = 1024;  // panel staged in smem when rows <= STAGE_ROWS
 constexpr int CW = 64;            // trailing-update column chunk
-constexpr int MAXK_T = 512;       // max columns when the full compact-WY T is formed
+constexpr int MAXK_T = 384;       // max columns when the full compact-WY T is formed
+constexpr int KPARTS = 4;         // row splits of W = Y^T X when tiles < warps
 
 struct QrSmem {
   double panel[STAGE_ROWS * NB];
@@ -24,6 +31,7 @@ struct QrSmem {
   double tcol[NB];
   double wc[NB * CW];
   double wc2[NB * CW];
+  double wpart[(KPARTS - 1) * NB * CW];
   double xs[MAXK_T * NB];   // X = Y[:,0:p0]^T Y_p, then X T_p (full-T merge)
   double red[32];
   double scal[4];
@@ -86,6 +94,112 @@ __device__ void panel_factor(double* P, int ldp, int rows, int pw, double* tau, 
       double v = 0.0;
       if (lane < j) {
         for (int a = lane; a < j; ++a) v = fma(S.tp[lane + a * NB], S.dmat[a * NB + j], v);
+      }
+      __syncwarp();
+      if (lane < j) S.tp[lane + j * NB] = -S.dv[j] * v;
+      if (lane == j) S.tp[j + j * NB] = S.dv[j];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// column j's reflector, formed by the warp that caches column j in `c`
+template <int E>
+__device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int lane, double* ybuf,
+                                           double* tau, QrSmem& S) {
+  double ss = 0.0, x0 = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane + 32 * e;
+    const double v = c[e];
+    if (i > j && i < rows) ss = fma(v, v, ss);
+    if (i == j) x0 = v;
+  }
+  ss = warp_sum(ss);
+  x0 = warp_sum(x0);
+  const double nrm = sqrt(x0 * x0 + ss);
+  double gamma = 0.0, rho = 0.0, inv = 0.0;
+  if (nrm != 0.0) {
+    const double sg = x0 < 0.0 ? -1.0 : 1.0;   // sign(0) := +1
+    const double u1 = x0 + sg * nrm;           // no cancellation
+    rho = -sg * nrm;
+    inv = 1.0 / u1;
+    gamma = 2.0 / (1.0 + ss * inv * inv);
+  }
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int i = lane + 32 * e;
+    if (i > j && i < rows) c[e] *= inv;
+    if (i == j) c[e] = rho;
+    ybuf[i] = i > j ? c[e] : (i == j ? 1.0 : 0.0);
+  }
+  if (lane == 0) { S.dv[j] = gamma; tau[j] = gamma; }
+}
+
+// Register-cached variant: warp w holds columns w and w+NW of the panel in
+// registers (lane l owns rows l, l+32, ...; E rows per lane), so a column
+// step is register arithmetic plus one shared-memory broadcast of y_j.
+template <int E>
+__device__ void panel_factor_reg(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  double col[2][E];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int c = wid + q * NW;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = lane + 32 * e;
+      col[q][e] = (c < pw && i < rows) ? P[i + (size_t)c * ldp] : 0.0;
+    }
+  }
+  double* ybuf = S.xs;  // broadcast buffer for y_j (rows <= 32 E)
+  for (int j = 0; j < pw; ++j) {
+    if (wid == (j % NW)) {
+      if (j < NW) own_column<E>(col[0], j, rows, lane, ybuf, tau, S);
+      else own_column<E>(col[1], j, rows, lane, ybuf, tau, S);
+    }
+    __syncthreads();
+    const double gamma = S.dv[j];
+    double y[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) y[e] = ybuf[lane + 32 * e];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = wid + q * NW;
+      if (c >= pw || c == j) continue;
+      double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; e += 2) {
+        d0 = fma(y[e], col[q][e], d0);
+        if (e + 1 < E) d1 = fma(y[e + 1], col[q][e + 1], d1);
+      }
+      const double d = warp_sum(d0 + d1);
+      if (c > j) {
+        const double gd = gamma * d;
+#pragma unroll
+        for (int e = 0; e < E; ++e) col[q][e] = fma(-gd, y[e], col[q][e]);
+      } else if (lane == 0) {
+        S.dmat[c * NB + j] = d;   // y_c^T y_j  (c < j)
+      }
+    }
+    __syncthreads();   // ybuf reused by the next column
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int c = wid + q * NW;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const int i = lane + 32 * e;
+      if (c < pw && i < rows) P[i + (size_t)c * ldp] = col[q][e];
+    }
+  }
+  // T (pw x pw): T[j][j] = gamma_j, T[0:j, j] = -gamma_j T[0:j,0:j] d[0:j, j]
+  if (wid == 0) {
+    for (int j = 0; j < pw; ++j) {
+      double v = 0.0;
+      if (lane < j) {
+        for (int a2 = lane; a2 < j; ++a2) v = fma(S.tp[lane + a2 * NB], S.dmat[a2 * NB + j], v);
       }
       __syncwarp();
       if (lane < j) S.tp[lane + j * NB] = -S.dv[j] * v;
@@ -164,8 +278,12 @@ __device__ void panel_factor_block(double* P, int ldp, int rows, int pw, double*
   }
 }
 
+// y_a(i) of panel reflector a (unit diagonal, zero above): the load is
+// unconditional (rows above the diagonal hold R, harmless) so a warp does
+// not diverge around it
 __device__ __forceinline__ double yval(const double* P, int ldp, int i, int a) {
-  return i == a ? 1.0 : (i > a ? P[i + (size_t)a * ldp] : 0.0);
+  const double v = P[i + (size_t)a * ldp];
+  return i > a ? v : (i == a ? 1.0 : 0.0);
 }
 
 // X (rows x ncols) := (I - Y T^op Y^T) X for panel reflectors Y (rows x pw,
@@ -180,31 +298,41 @@ __device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, con
   const int gq = lane >> 2, tq = lane & 3;
   for (int c0 = 0; c0 < ncols; c0 += CW) {
     const int cw = min(CW, ncols - c0);
-    // ---- W = Y^T X_chunk : 2 x (CW/8) output tiles of 8x8
-    for (int tile = wid; tile < 2 * (CW / 8); tile += NW) {
+    // ---- W = Y^T X_chunk : 2 x ntn output tiles of 8x8; when there are fewer
+    // tiles than warps the row range is split and the partials summed
+    const int ntn = (cw + 7) / 8, tiles = 2 * ntn;
+    const int kparts = max(1, min(KPARTS, NW / tiles));
+    const int kchunk = ((rows + kparts - 1) / kparts + 31) & ~31;
+    for (int item = wid; item < tiles * kparts; item += NW) {
+      const int tile = item % tiles, kp = item / tiles;
       const int mt = tile & 1, nt = tile >> 1;
-      if (nt * 8 >= cw) continue;
       double d0 = 0.0, d1 = 0.0;
       const int a = mt * 8 + gq;          // A row  (reflector index)
       const int j = nt * 8 + gq;          // B col  (chunk column)
       const double* xc = X + (size_t)(c0 + j) * ldx;
+      const int kb = kp * kchunk, ke = min(rows, kb + kchunk);
       // loads for 8 k-steps issued back to back, then 8 DMMAs (latency hiding)
-      for (int k0 = 0; k0 < rows; k0 += 32) {
+      for (int k0 = kb; k0 < ke; k0 += 32) {
         double av[8], bv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int ia = k0 + 4 * u + tq;
-          av[u] = (ia < rows && a < pw) ? yval(Y, ldy, ia, a) : 0.0;
-          bv[u] = (ia < rows && j < cw) ? xc[ia] : 0.0;
+          av[u] = (ia < ke && a < pw) ? yval(Y, ldy, ia, a) : 0.0;
+          bv[u] = (ia < ke && j < cw) ? xc[ia] : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
       }
       const int r = mt * 8 + gq, cc = nt * 8 + 2 * tq;
-      S.wc[r + cc * NB] = d0;
-      S.wc[r + (cc + 1) * NB] = d1;
+      double* wp = kp == 0 ? S.wc : S.wpart + (kp - 1) * NB * CW;
+      wp[r + cc * NB] = d0;
+      wp[r + (cc + 1) * NB] = d1;
     }
     __syncthreads();
+    if (kparts > 1)
+      for (int e = t; e < NB * cw; e += NT)
+        for (int kp = 1; kp < kparts; ++kp) S.wc[e] += S.wpart[(kp - 1) * NB * CW + e];
+    if (kparts > 1) __syncthreads();
     for (int e = t; e < NB * cw; e += NT) {
       const int a = e % NB, cc = e / NB;
       double v = 0.0;
@@ -215,64 +343,61 @@ __device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, con
       S.wc2[a + cc * NB] = v;
     }
     __syncthreads();
-    // ---- X_chunk -= Y W2 : (rows/8) x (cw/8) tiles, k = NB
-    const int ntm = (rows + 7) / 8, ntn = (cw + 7) / 8;
-    for (int tile = wid; tile < ntm * ntn; tile += NW) {
-      const int mt = tile % ntm, nt = tile / ntm;
-      const int i = mt * 8 + gq;              // output row
-      const int j = nt * 8 + 2 * tq;          // output cols j, j+1
-      double* x0 = X + (size_t)(c0 + j) * ldx;
-      double* x1 = x0 + ldx;
-      double d0 = (i < rows && j < cw) ? x0[i] : 0.0;
-      double d1 = (i < rows && j + 1 < cw) ? x1[i] : 0.0;
-      const int ib = mt * 8 + gq;             // A row for the fragment
-      const int jb = nt * 8 + gq;             // B col for the fragment
+    // ---- X_chunk -= Y W2 : (rows/8) x (cw/8) tiles, k = NB; four tiles per
+    // warp iteration with all their loads issued before the DMMAs
+    const int ntm = (rows + 7) / 8, ntt = ntm * ntn;
+    for (int base = wid; base < ntt; base += 4 * NW) {
+      double d0[4], d1[4], av[4][4], bv[4][4];
 #pragma unroll
-      for (int k0 = 0; k0 < NB; k0 += 4) {
-        const int a = k0 + tq;
-        const double av = (ib < rows && a < pw) ? -yval(Y, ldy, ib, a) : 0.0;
-        const double bv = (jb < cw) ? S.wc2[a + jb * NB] : 0.0;
-        dmma884(d0, d1, av, bv);
+      for (int u = 0; u < 4; ++u) {
+        const int tile = base + u * NW;
+        const bool ok = tile < ntt;
+        const int mt = ok ? tile % ntm : 0, nt = ok ? tile / ntm : 0;
+        const int i = mt * 8 + gq, j = nt * 8 + 2 * tq;
+        const double* x0 = X + (size_t)(c0 + j) * ldx;
+        d0[u] = (ok && i < rows && j < cw) ? x0[i] : 0.0;
+        d1[u] = (ok && i < rows && j + 1 < cw) ? x0[ldx + i] : 0.0;
+        const int ib = mt * 8 + gq, jb = nt * 8 + gq;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int a = 4 * q + tq;
+          av[u][q] = (ok && ib < rows && a < pw) ? -yval(Y, ldy, ib, a) : 0.0;
+          bv[u][q] = (ok && jb < cw) ? S.wc2[a + jb * NB] : 0.0;
+        }
       }
-      if (i < rows && j < cw) x0[i] = d0;
-      if (i < rows && j + 1 < cw) x1[i] = d1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(d0[u], d1[u], av[u][q], bv[u][q]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int tile = base + u * NW;
+        if (tile >= ntt) continue;
+        const int mt = tile % ntm, nt = tile / ntm;
+        const int i = mt * 8 + gq, j = nt * 8 + 2 * tq;
+        double* x0 = X + (size_t)(c0 + j) * ldx;
+        if (i < rows && j < cw) x0[i] = d0[u];
+        if (i < rows && j + 1 < cw) x0[ldx + i] = d1[u];
+      }
     }
     __syncthreads();
   }
 }
 
-// Factor panel p0 of problem Q: stage it (when it fits), reduce it, publish
-// gamma / T_p, (single-CTA path: update the trailing columns while the
-// panel is staged), merge T_p into the full compact-WY T when requested,
-// write the panel back.
-__device__ void factor_panel_step(const hq_qr_prob& Q, double* W, int ld, int m, int k, int r, int p0,
-                                  bool do_trailing, QrSmem& S) {
+// Merge panel p0 (reflectors P, ld ldp; T factor tp) into the full
+// compact-WY T: T[0:p0, p] = -T[0:p0,0:p0] (Y[:,0:p0]^T Y_p) T_p (wy.py:53).
+// Needs the T blocks of all earlier panels.
+__device__ void merge_T(const hq_qr_prob& Q, const double* W, int ld, int m, int r, int p0,
+                        const double* P, int ldp, const double* tpv, QrSmem& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int pw = min(NB, r - p0), rows = m - p0;
+  const double* tp_ = tpv;
   {
-    const int pw = min(NB, r - p0), rows = m - p0;
-    double* Pg = W + p0 + (size_t)p0 * ld;
-    const bool staged = rows <= STAGE_ROWS;
-    double* P = Pg;
-    int ldp = ld;
-    if (staged) {
-      P = S.panel; ldp = rows;
-      for (int e = t; e < rows * pw; e += NT) P[e % rows + (e / rows) * ldp] = Pg[e % rows + (size_t)(e / rows) * ld];
-    }
-    if (t < NB * NB) S.tp[t] = 0.0;
-    __syncthreads();
-    if (staged) panel_factor(P, ldp, rows, pw, Q.tau + p0, S);
-    else panel_factor_block(P, ldp, rows, pw, Q.tau + p0, S);
-    if (Q.tpanel && t < NB * NB) Q.tpanel[(size_t)(p0 / NB) * NB * NB + t] = S.tp[t];
-    // trailing columns: A_trail := Q_p^T A_trail
-    if (do_trailing && p0 + pw < k)
-      apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S);
-    __syncthreads();
-    // full compact-WY T: T[0:p0, p] = -T[0:p0,0:p0] (Y[:,0:p0]^T Y_p) T_p   (wy.py:53)
     if (Q.tfull) {
       double* TF = Q.tfull;
       const int ldt = Q.ldt;
       const int gq = lane >> 2, tq = lane & 3;
-      for (int e = t; e < pw * pw; e += NT) TF[(p0 + e % pw) + (size_t)(p0 + e / pw) * ldt] = S.tp[e % pw + (e / pw) * NB];
+      for (int e = t; e < pw * pw; e += NT) TF[(p0 + e % pw) + (size_t)(p0 + e / pw) * ldt] = tp_[e % pw + (e / pw) * NB];
       if (p0 > 0) {
         // X (p0 x NB) = Y[:,0:p0]^T Y_p over local rows 0..rows-1 (DMMA)
         const int ntm = (p0 + 7) / 8;
@@ -305,7 +430,7 @@ __device__ void factor_panel_step(const hq_qr_prob& Q, double* W, int ld, int m,
             double v = 0.0;
 #pragma unroll
             for (int c = 0; c < NB; ++c)
-              if (c <= a) v = fma(xr[c], S.tp[c + a * NB], v);
+              if (c <= a) v = fma(xr[c], tp_[c + a * NB], v);
             if (a < pw) S.xs[b + a * MAXK_T] = v;
           }
         }
@@ -333,6 +458,40 @@ __device__ void factor_panel_step(const hq_qr_prob& Q, double* W, int ld, int m,
       }
       __syncthreads();
     }
+  }
+}
+
+// Factor panel p0 of problem Q: stage it (when it fits), reduce it, publish
+// gamma / T_p, (single-CTA path: update the trailing columns while the
+// panel is staged), merge T_p into the full compact-WY T when requested,
+// write the panel back.
+__device__ void factor_panel_step(const hq_qr_prob& Q, double* W, int ld, int m, int k, int r, int p0,
+                                  bool do_trailing, bool do_merge, QrSmem& S) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  {
+    const int pw = min(NB, r - p0), rows = m - p0;
+    double* Pg = W + p0 + (size_t)p0 * ld;
+    const bool staged = rows <= STAGE_ROWS;
+    double* P = Pg;
+    int ldp = ld;
+    if (staged) {
+      P = S.panel; ldp = rows;
+      for (int e = t; e < rows * pw; e += NT) P[e % rows + (e / rows) * ldp] = Pg[e % rows + (size_t)(e / rows) * ld];
+    }
+    if (t < NB * NB) S.tp[t] = 0.0;
+    __syncthreads();
+    if (rows <= 128) panel_factor_reg<4>(P, ldp, rows, pw, Q.tau + p0, S);
+    else if (rows <= 256) panel_factor_reg<8>(P, ldp, rows, pw, Q.tau + p0, S);
+    else if (rows <= 512) panel_factor_reg<16>(P, ldp, rows, pw, Q.tau + p0, S);
+    else if (rows <= 1024) panel_factor_reg<32>(P, ldp, rows, pw, Q.tau + p0, S);
+    else if (staged) panel_factor(P, ldp, rows, pw, Q.tau + p0, S);
+    else panel_factor_block(P, ldp, rows, pw, Q.tau + p0, S);
+    if (Q.tpanel && t < NB * NB) Q.tpanel[(size_t)(p0 / NB) * NB * NB + t] = S.tp[t];
+    // trailing columns: A_trail := Q_p^T A_trail
+    if (do_trailing && p0 + pw < k)
+      apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S);
+    __syncthreads();
+    if (do_merge) merge_T(Q, W, ld, m, r, p0, P, ldp, S.tp, S);
     if (staged) {
       for (int e = t; e < rows * pw; e += NT) Pg[e % rows + (size_t)(e / rows) * ld] = P[e % rows + (e / rows) * ldp];
     }
@@ -347,7 +506,7 @@ __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ p
   const hq_qr_prob Q = probs[blockIdx.x];
   const int m = hq_dim(rank, Q.m, Q.m_ri), k = hq_dim(rank, Q.k, Q.k_ri);
   const int r = m < k ? m : k;
-  for (int p0 = 0; p0 < r; p0 += NB) factor_panel_step(Q, Q.w, Q.ldw, m, k, r, p0, true, S);
+  for (int p0 = 0; p0 < r; p0 += NB) factor_panel_step(Q, Q.w, Q.ldw, m, k, r, p0, true, true, S);
 }
 
 // Householder QR of one problem on a G-CTA cluster.  Column blocks of NB are
@@ -370,7 +529,13 @@ __global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __r
   const int np = (r + NB - 1) / NB, nbk = (k + NB - 1) / NB;
   double* W = Q.w;
   const int ld = Q.ldw;
+#ifdef HQ_DEBUG_TIMING
+  long long tph = clock64();
+#endif
   for (int ph = 0; ph <= np; ++ph) {
+#ifdef HQ_DEBUG_TIMING
+    long long tA = clock64(), tB = tA, tC = tA;
+#endif
     if (ph >= 1) {
       const int q0 = (ph - 1) * NB, qw = min(NB, r - q0), rows = m - q0;
       if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
@@ -392,17 +557,39 @@ __global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __r
           apply_panel_cols(Y, ld, rows, qw, S.tp, W + q0 + (size_t)c0 * ld, ld, cw, true, S);
         }
         if (pass == 0 && ph < np && (ph % G) == cr) {
-          factor_panel_step(Q, W, ld, m, k, r, ph * NB, false, S);
+#ifdef HQ_DEBUG_TIMING
+          tB = clock64();
+#endif
+          factor_panel_step(Q, W, ld, m, k, r, ph * NB, false, false, S);
+#ifdef HQ_DEBUG_TIMING
+          tC = clock64();
+#endif
           // factoring overwrote S.tp with T_ph: restore T_(ph-1) for pass 1
           if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
           __syncthreads();
         }
       }
+      // the full compact-WY T block of panel ph-1 is merged one phase later
+      // by a CTA that is not factoring (off the panel chain)
+      if (Q.tfull && cr == (ph + 1) % G) {
+        __syncthreads();
+        merge_T(Q, W, ld, m, r, q0, Y, ld, S.tp, S);
+      }
     } else if (np > 0 && cr == 0) {
-      factor_panel_step(Q, W, ld, m, k, r, 0, false, S);
+      factor_panel_step(Q, W, ld, m, k, r, 0, false, false, S);
     }
     __syncthreads();
+#ifdef HQ_DEBUG_TIMING
+    long long tD = clock64();
+#endif
     cluster.sync();
+#ifdef HQ_DEBUG_TIMING
+    long long tE = clock64();
+    if (threadIdx.x == 0 && blockIdx.x < 8 && ph < 64 && hq_dbg) {
+      long long* d = hq_dbg + (blockIdx.x * 64 + ph) * 4;
+      d[0] = tB - tA; d[1] = tC - tB; d[2] = tD - tC; d[3] = tE - tD;
+    }
+#endif
   }
 }
 
@@ -410,6 +597,7 @@ struct ApqSmem {
   double tp[NB * NB];
   double wc[NB * CW];
   double wc2[NB * CW];
+  double wpart[(KPARTS - 1) * NB * CW];
 };
 
 // grid (problem, column chunk of APQ_CW): the columns of X are independent,

@@ -508,8 +508,8 @@ class Builder:
         self.lane = 0
         self.lane_bump(R_PHASE).reset()
         nl = t.size[v]
-        if nl > 512:
-            raise ValueError("leaf blocks larger than 512 are not supported by the leaf QR kernel")
+        if nl > 384:
+            raise ValueError("leaf blocks larger than 384 are not supported by the leaf QR kernel")
         gat, qr = [], []
         for b in range(self.B):
             d = self.lay.m[b]

@@ -58,3 +58,40 @@ for i, (kind, probs, ex) in enumerate(ops):
     agg[key][0] += times[i]; agg[key][1] += 1
 for k, (tm, c) in sorted(agg.items(), key=lambda x: -x[1][0]):
     print(f"{k:32s} {c:5d} launches {tm:9.1f} ms")
+# critical path through the DAG (per-op times from this serialized pass)
+from paper_1809_10585_b200.plan import op_resources
+lanes = plan.lanes
+finish = [0.0] * len(ops)
+pred = [-1] * len(ops)
+last_in_lane = {}
+last_w, readers = {}, {}
+for i, (kind, probs, ex) in enumerate(ops):
+    Rs, Ws = op_resources(eng.builder, kind, probs, ex)
+    deps = set()
+    for r in Rs | Ws:
+        if r in last_w: deps.add(last_w[r])
+    for r in Ws: deps.update(readers.get(r, ()))
+    ln = lanes[i]
+    if ln in last_in_lane: deps.add(last_in_lane[ln])
+    best = max(deps, key=lambda d: finish[d], default=-1)
+    finish[i] = (finish[best] if best >= 0 else 0.0) + times[i]
+    pred[i] = best
+    last_in_lane[ln] = i
+    for r in Rs: readers.setdefault(r, []).append(i)
+    for r in Ws: last_w[r] = i; readers[r] = []
+end = max(range(len(ops)), key=lambda i: finish[i])
+print(f"critical path {finish[end]:.1f} ms (serialized sum {sum(times):.1f} ms)")
+cp = collections.defaultdict(lambda: [0.0, 0])
+i = end
+while i >= 0:
+    kind, probs, ex = ops[i]
+    key = kind
+    if kind == "qr" and probs:
+        mm = max(_dv(p[6], rk) for p in probs)
+        key = f"qr {'leaf' if probs[0][3] is not None else 'trunc'} m{'<=512' if mm <= 512 else ('<=1024' if mm <= 1024 else '>1024')}"
+    elif kind == "svd":
+        key = f"svd cl{ex.get('cluster',1)}"
+    cp[key][0] += times[i]; cp[key][1] += 1
+    i = pred[i]
+for k, (tm, c) in sorted(cp.items(), key=lambda x: -x[1][0]):
+    print(f"  on path: {k:28s} {c:5d} ops {tm:9.1f} ms")
