@@ -152,6 +152,21 @@ typedef struct hq_copy_item {
   int32_t pad_;
 } hq_copy_item;
 
+/* TSQR row blocks of a tall factor stack W (rows_total x K, chunks of ch rows
+   QR'd in place): mode 0 stacks each chunk's R (its top min(rows_c, K) rows,
+   upper part) densely into S (rank[ms_ri] = stacked row count); mode 1
+   scatters the matching row blocks of S back to the chunk tops of X (= W
+   argument, ncol columns) and zero-fills the rest of every chunk */
+typedef struct hq_rowblk_prob {
+  double* s;
+  double* w;
+  int32_t lds, ldw;
+  int32_t ch, rows_total;
+  int32_t k, k_ri;
+  int32_t ncol, ncol_ri;
+  int32_t ms_ri, mode;
+} hq_rowblk_prob;
+
 /* ---- launchers ---------------------------------------------------------- */
 int hq_abi_version(void);
 int hq_device_check(void);
@@ -184,6 +199,7 @@ int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob, const hq
 int hq_copy(void* stream, const hq_copy_item* items, int nitem, const int* rank);
 int hq_pack_offsets(void* stream, hq_copy_item* items, int nitem, const int* rank, double* base,
                     int64_t* total, int which);
+int hq_rowblocks(void* stream, const hq_rowblk_prob* probs, int nprob, int* rank, int max_chunks);
 /* zero a list of (ptr, count) regions: regions[2i] = ptr, regions[2i+1] = count */
 int hq_zero(void* stream, const int64_t* regions, int nregion, int64_t max_count);
 /* one step of the two-vector power iteration for ||A||_2 (dense.py:102-141),

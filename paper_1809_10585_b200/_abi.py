@@ -44,14 +44,18 @@ LEAF_PROB = np.dtype([("leaf", P), ("panel", P), ("nl", I), ("ldp", I), ("slab0"
 COPY_ITEM = np.dtype([("src", P), ("dst", P), ("rows", I), ("cols", I), ("cols_ri", I),
                       ("lds", I), ("ldd", I), ("pad_", I)], align=True)
 
-STRUCT_SIZES = {"hq_copy_item": COPY_ITEM, "hq_gemm_term": GEMM_TERM, "hq_gemm_prob": GEMM_PROB, "hq_piece": PIECE,
+ROWBLK_PROB = np.dtype([("s", P), ("w", P), ("lds", I), ("ldw", I), ("ch", I), ("rows_total", I),
+                        ("k", I), ("k_ri", I), ("ncol", I), ("ncol_ri", I), ("ms_ri", I),
+                        ("mode", I)], align=True)
+
+STRUCT_SIZES = {"hq_rowblk_prob": ROWBLK_PROB, "hq_copy_item": COPY_ITEM, "hq_gemm_term": GEMM_TERM, "hq_gemm_prob": GEMM_PROB, "hq_piece": PIECE,
                 "hq_concat_prob": CONCAT_PROB, "hq_qr_prob": QR_PROB,
                 "hq_applyq_prob": APPLYQ_PROB, "hq_svd_prob": SVD_PROB, "hq_slab": SLAB,
                 "hq_leaf_prob": LEAF_PROB}
 
 EXPORTS = ("hq_abi_version", "hq_device_check", "hq_gemm", "hq_concat", "hq_qr", "hq_applyq",
            "hq_svd", "hq_leaf_gather", "hq_leaf_scatter", "hq_zero", "hq_power_step", "hq_copy",
-           "hq_pack_offsets")
+           "hq_pack_offsets", "hq_rowblocks")
 
 _vp, _i, _d, _i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
 SIGNATURES = {
@@ -67,6 +71,7 @@ SIGNATURES = {
     "hq_zero": [_vp, _vp, _i, _i64],
     "hq_copy": [_vp, _vp, _i, _vp],
     "hq_pack_offsets": [_vp, _vp, _i, _vp, _vp, _vp, _i],
+    "hq_rowblocks": [_vp, _vp, _i, _vp, _i],
     "hq_power_step": [_vp, _vp, _vp, _vp, _i, _i, _vp, _d, _d, _vp, _vp, _i, _i],
 }
 

@@ -751,6 +751,32 @@ __global__ void pack_offsets_kernel(hq_copy_item* items, int nitem, const int* r
   if (threadIdx.x == 0) total[0] = carry;
 }
 
+__global__ void rowblk_kernel(const hq_rowblk_prob* __restrict__ probs, int* __restrict__ rank) {
+  const hq_rowblk_prob B = probs[blockIdx.y];
+  const int c = blockIdx.x;
+  const int nch = (B.rows_total + B.ch - 1) / B.ch;
+  if (c >= nch) return;
+  const int K = hq_dim(rank, B.k, B.k_ri);
+  // stacked offset of chunk c: every full chunk contributes min(ch, K) rows
+  const int kr_full = min(B.ch, K);
+  const int off = c * kr_full;
+  const int rows_c = min(B.ch, B.rows_total - c * B.ch);
+  const int kr = min(rows_c, K);
+  if (B.mode == 0) {
+    for (int e = threadIdx.x; e < kr * K; e += blockDim.x) {
+      const int a = e % kr, b = e / kr;
+      B.s[(off + a) + (size_t)b * B.lds] = a <= b ? B.w[(c * B.ch + a) + (size_t)b * B.ldw] : 0.0;
+    }
+    if (c == nch - 1 && threadIdx.x == 0) rank[B.ms_ri] = off + kr;
+  } else {
+    const int nc = hq_dim(rank, B.ncol, B.ncol_ri);
+    for (int e = threadIdx.x; e < rows_c * nc; e += blockDim.x) {
+      const int i = e % rows_c, j = e / rows_c;
+      B.w[(c * B.ch + i) + (size_t)j * B.ldw] = i < kr ? B.s[(off + i) + (size_t)j * B.lds] : 0.0;
+    }
+  }
+}
+
 bool g_attr_done = false;
 }  // namespace
 
@@ -849,5 +875,12 @@ extern "C" int hq_pack_offsets(void* stream, hq_copy_item* items, int nitem, con
                                double* base, int64_t* total, int which) {
   if (nitem <= 0) return 0;
   pack_offsets_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(items, nitem, rank, base, total, which);
+  return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_rowblocks(void* stream, const hq_rowblk_prob* probs, int nprob, int* rank,
+                            int max_chunks) {
+  if (nprob <= 0 || max_chunks <= 0) return 0;
+  rowblk_kernel<<<dim3(max_chunks, nprob), 256, 0, (cudaStream_t)stream>>>(probs, rank);
   return hq_err(cudaGetLastError());
 }

@@ -35,6 +35,8 @@ from . import _abi
 from .hodlr import PartitionTree
 
 NB = 16          # QR panel width (hq_qr.cu)
+TALL_ROWS = 1024  # factor stacks taller than this are QR'd by one-level TSQR
+TSQR_CH = 512     # TSQR chunk rows (register-cached panels)
 GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
 SVD_MAX_N = 1024
 
@@ -381,8 +383,34 @@ class Builder:
             return
         z = self.lane_bump(R_TRUNC)
         z.reset()
-        cat, cat_pieces, qr, gm_c, qrc, svd, apq, gm_m, gm_v = [], [], [], [], [], [], [], [], []
-        maxrows = 0
+        cat, qr, stack, qrs, gm_c, qrc, svd, apq, unstack, apq2, gm_m, gm_v = ([] for _ in range(12))
+        maxrows, maxch = 0, 0
+
+        def factor_side(W, rows, kcap, kri, tau, tp):
+            """QR of a factor stack; tall stacks (rows > TALL_ROWS) go through a
+            one-level TSQR: chunk QRs in parallel, their R's stacked densely
+            (hq_rowblocks), QR of the stack.  Returns the R source (buf, ld)
+            and the chunk description for the Q application."""
+            nonlocal maxch
+            if rows <= TALL_ROWS:
+                qr.append((W, tau, tp, None, rows, 0, Dim(rows), Dim(kcap, kri)))
+                return (W, rows), None
+            nch = math.ceil(rows / TSQR_CH)
+            maxch = max(maxch, nch)
+            npan = max(1, math.ceil(kcap / NB))
+            chunks = []
+            for c in range(nch):
+                rc = min(TSQR_CH, rows - c * TSQR_CH)
+                tc, pc = z.alloc(kcap), z.alloc(npan * NB * NB)
+                qr.append((W + c * TSQR_CH, tc, pc, None, rows, 0, Dim(rc), Dim(kcap, kri)))
+                chunks.append((c * TSQR_CH, rc, tc, pc))
+            srows = nch * min(TSQR_CH, kcap)
+            S, tS, pS = z.alloc(srows * kcap), z.alloc(kcap), z.alloc(npan * NB * NB)
+            ms = self.slots.take()
+            stack.append((S, W, srows, rows, TSQR_CH, rows, Dim(kcap, kri), Dim(0), ms, 0))
+            qrs.append((S, tS, pS, None, srows, 0, Dim(srows, ms), Dim(kcap, kri)))
+            return (S, srows), dict(S=S, srows=srows, tS=tS, pS=pS, ms=ms, chunks=chunks, W=W, rows=rows)
+
         for p in probs:
             m, n, cap = p["m"], p["n"], p["cap"]
             kcap = sum(d.cap for _, _, d, _ in p["L"])
@@ -400,30 +428,48 @@ class Builder:
             cat.append((WL, None, m, kL, p["L"]))
             cat.append((WR, WRc, n, kR, p["R"]))
             maxrows = max(maxrows, m, n)
-            qr.append((WL, tauL, tpL, None, m, 0, Dim(m), Dim(kcap, kL)))
-            qr.append((WR, tauR, tpR, None, n, 0, Dim(n), Dim(kcap, kR)))
+            (R1, ld1), tsL = factor_side(WL, m, kcap, kL, tauL, tpL)
+            (R2, ld2), _ = factor_side(WR, n, kcap, kR, tauR, tpR)
             # C^T = R2 R1^T (masks: upper on the stored R factors); its QR gives
             # the LQ preconditioner X = R_c^T of C (Jacobi converges in few sweeps)
             gm_c.append((C, k2, Dim(k2, kR), Dim(k1, kL), 0.0,
-                         [(WR, n, 0, 1, WL, m, 1, 1, Dim(kcap, kL), 1.0)]))
+                         [(R2, ld2, 0, 1, R1, ld1, 1, 1, Dim(kcap, kL), 1.0)]))
             qrc.append((C, tauC, tpC, None, k2, 0, Dim(k2, kR), Dim(k1, kL)))
             svd.append((C, Uk, Xw, k2, k1, Dim(k1, kL), Dim(k2, kR), cap, p["rank_ri"],
                         self.flag_slot, p["eps_slot"], p["eps_scale"], 1))
             U, ldu = p["U"]
             V, ldv = p["V"]
-            apq.append((WL, tauL, tpL, U, Uk, m, ldu, k1, Dim(m), Dim(kcap, kL),
-                        Dim(cap, p["rank_ri"]), Dim(k1, kL), 0))
+            if tsL is None:
+                apq.append((WL, tauL, tpL, U, Uk, m, ldu, k1, Dim(m), Dim(kcap, kL),
+                            Dim(cap, p["rank_ri"]), Dim(k1, kL), 0))
+            else:
+                # L_out = blockdiag(Q_c) Q_S [U_k; 0]
+                srows = tsL["srows"]
+                Z = z.alloc(srows * cap)
+                apq.append((tsL["S"], tsL["tS"], tsL["pS"], Z, Uk, srows, srows, k1,
+                            Dim(srows, tsL["ms"]), Dim(kcap, kL), Dim(cap, p["rank_ri"]),
+                            Dim(k1, kL), 0))
+                unstack.append((Z, U, srows, ldu, TSQR_CH, m, Dim(kcap, kL), Dim(cap, p["rank_ri"]), -1, 1))
+                for (r0, rc, tc, pc) in tsL["chunks"]:
+                    apq2.append((WL + r0, tc, pc, U + r0, None, m, ldu, 0, Dim(rc), Dim(kcap, kL),
+                                 Dim(cap, p["rank_ri"]), Dim(0), 0))
             # Mm = R1^T U_k ; V = WRc Mm  (right factor = P^T L_out, no 1/sigma)
             gm_m.append((Mm, kcap, Dim(kcap, kL), Dim(cap, p["rank_ri"]), 0.0,
-                         [(WL, m, 1, 1, Uk, k1, 0, 0, Dim(k1, kL), 1.0)]))
+                         [(R1, ld1, 1, 1, Uk, k1, 0, 0, Dim(k1, kL), 1.0)]))
             gm_v.append((V, ldv, Dim(n), Dim(cap, p["rank_ri"]), 0.0,
                          [(WRc, n, 0, 0, Mm, kcap, 0, 0, Dim(kcap, kL), 1.0)]))
         self.op("concat", cat, dict(max_rows=maxrows))
         self.op("qr", qr)
+        if stack:
+            self.op("rowblk", stack, dict(max_chunks=maxch))
+            self.op("qr", qrs)
         self.gemm(gm_c)
         self.op("qr", qrc)
         self.op("svd", svd, svd_cluster(svd))
         self.op("applyq", apq, dict(max_cols=max(p[10].cap for p in apq)))
+        if unstack:
+            self.op("rowblk", unstack, dict(max_chunks=maxch))
+            self.op("applyq", apq2, dict(max_cols=max(p[10].cap for p in apq2)))
         self.gemm(gm_m)
         self.gemm(gm_v)
 
@@ -839,6 +885,13 @@ def op_resources(builder, kind, probs, extra):
             slot(builder.power_done + i), slot(builder.power_done + i, True)
         for i in (0, 1):
             slot(builder.all_done + i), slot(builder.all_done + i, True)
+    elif kind == "rowblk":
+        for (S_, W_, lds, ldw, ch, rt, k, nc, msr, mode) in probs:
+            slot(k), slot(nc)
+            if mode == 0:
+                rd(W_), wr(S_), slot(msr, True)
+            else:
+                rd(S_), wr(W_)
     elif kind == "pack_copy":
         if extra["which"] == 1:
             rd(Buf(R_IN, 0))
@@ -976,6 +1029,11 @@ class CompiledPlan:
                 self.launch.append((kind, put(pa), put(sa), len(probs), extra))
             elif kind == "power":
                 self.launch.append(("power", None, None, builder.B, extra))
+            elif kind == "rowblk":
+                pa = np.zeros(len(probs), _abi.ROWBLK_PROB)
+                for i, (S_, W_, lds, ldw, ch, rt, k, nc, msr, mode) in enumerate(probs):
+                    pa[i] = (A(S_), A(W_), lds, ldw, ch, rt, k.cap, k.ri, nc.cap, nc.ri, msr, mode)
+                self.launch.append(("rowblk", put(pa), None, len(probs), extra))
             elif kind == "pack_copy":
                 it = np.zeros(len(probs), _abi.COPY_ITEM)
                 for i, (buf, rows, cols) in enumerate(probs):
@@ -1050,6 +1108,8 @@ class CompiledPlan:
                 rc = lib.hq_leaf_gather(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
             elif kind == "leaf_scatter":
                 rc = lib.hq_leaf_scatter(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
+            elif kind == "rowblk":
+                rc = lib.hq_rowblocks(stream_handle, dp + o1, cnt, rk, ex["max_chunks"])
             elif kind == "pack_copy":
                 rc = lib.hq_pack_offsets(stream_handle, dp + o1, cnt, rk, ex["base_ptr"],
                                          self.totals.data_ptr() + 8 * ex["total"], ex["which"])

@@ -241,6 +241,30 @@ class Emu:
             x[:] = np.linalg.qr(np.array(w))[0]
             self.scal[2 * i] = est
 
+    def rowblk(self, o1, cnt, ex):
+        for B in self.arr(o1, _abi.ROWBLK_PROB, cnt):
+            K = self.dim(B["k"], B["k_ri"])
+            ch, rt = int(B["ch"]), int(B["rows_total"])
+            nch = -(-rt // ch)
+            krf = min(ch, K)
+            for c in range(nch):
+                off = c * krf
+                rows_c = min(ch, rt - c * ch)
+                kr = min(rows_c, K)
+                if B["mode"] == 0:
+                    if kr and K:
+                        src = np.triu(np.array(self.mat(B["w"] + 8 * c * ch, B["ldw"], kr, K)))
+                        self.mat(B["s"] + 8 * off, B["lds"], kr, K)[:] = src
+                    if c == nch - 1:
+                        self.rank[B["ms_ri"]] = off + kr
+                else:
+                    nc = self.dim(B["ncol"], B["ncol_ri"])
+                    if nc:
+                        blk = np.zeros((rows_c, nc))
+                        if kr:
+                            blk[:kr] = self.mat(B["s"] + 8 * off, B["lds"], kr, nc)
+                        self.mat(B["w"] + 8 * c * ch, B["ldw"], rows_c, nc)[:] = blk
+
     def pack_copy(self, o1, cnt, ex):
         items = self.arr(o1, _abi.COPY_ITEM, cnt)
         base = ex["base_ptr"]
@@ -307,6 +331,8 @@ class Emu:
                 self.power(ex)
             elif kind == "pack_copy":
                 self.pack_copy(o1, cnt, ex)
+            elif kind == "rowblk":
+                self.rowblk(o1, cnt, ex)
             else:
                 raise ValueError(kind)
 

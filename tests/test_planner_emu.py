@@ -70,3 +70,18 @@ def test_multistream_schedule_is_hazard_free(seed):
     for k in ("y", "t", "r"):
         d0, d1 = to_dense(getattr(f0, k)), to_dense(getattr(f1, k))
         assert np.abs(d0 - d1).max() <= 1e-12 * max(1.0, np.abs(d0).max())
+
+
+def test_tsqr_path_for_tall_factor_stacks(monkeypatch):
+    """Force the one-level TSQR branch (chunk QRs, stacked R's, Q applied in
+    two stages) on a small case and compare with the oracle."""
+    import paper_1809_10585_b200.plan as PL
+    monkeypatch.setattr(PL, "TALL_ROWS", 40)
+    monkeypatch.setattr(PL, "TSQR_CH", 24)
+    a = gen.gen_random_hodlr(256, 32, 4, 8.0, seed=0)
+    (f,), io, plan = emulate([a], 1e-10)
+    assert any(op[0] == "rowblk" for op in plan.launch)
+    y, t, r = O.hqr(a, 1e-10)
+    assert np.linalg.norm(to_dense(f.r) - to_dense(r)) <= 1e-8 * np.linalg.norm(to_dense(r))
+    e_orth, e_acc = O.dense_metrics(to_dense(a), f.y, f.t, f.r)
+    assert e_orth <= 1e-13 and e_acc <= 1e-11
