@@ -12,6 +12,8 @@ constexpr int MAX_SWEEPS = 40;
 struct SvdSmem {
   double cs[SMEM_DOUBLES];
   double nrm[MAX_N];
+  short act[MAX_N];   // active columns (compaction of negligible ones)
+  int nact;
   double g[MAX_N / 2];
   double rc[MAX_N / 2];
   double rs[MAX_N / 2];
@@ -39,23 +41,49 @@ __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, doubl
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int grp = wid * GPW + lane / LP, gl = lane % LP;
   const int ngroups = NW * GPW;
-  const int np = n + (n & 1), N = np - 1, npair = np / 2;
+  for (int j = t; j < n; j += NT) S.act[j] = (short)j;
+  if (t == 0) S.nact = n;
+  __syncthreads();
   int sweep = 0;
-  for (; sweep < MAX_SWEEPS && N > 0; ++sweep) {
-    for (int j = wid; j < n; j += NW) {
+  for (; sweep < MAX_SWEEPS; ++sweep) {
+    const int nact0 = S.nact;
+    for (int jj = wid; jj < nact0; jj += NW) {
+      const int j = S.act[jj];
       const double* xj = X + (size_t)j * ld;
       double v = 0.0;
       for (int i = lane; i < m; i += 32) v = fma(xj[i], xj[i], v);
       v = warp_sum(v);
       if (lane == 0) S.nrm[j] = v;
     }
+    __syncthreads();
+    // after the first sweep, columns far below the threshold (norm < 1e-3 thr)
+    // leave the rotation set: they are dropped by the truncation and moving
+    // them changes the kept columns by less than that
+    if (sweep >= 1 && t == 0) {
+      int k = 0;
+      for (int jj = 0; jj < nact0; ++jj) {
+        const int j = S.act[jj];
+        if (!(S.nrm[j] < tiny2)) S.act[k++] = (short)j;
+      }
+      S.nact = k;
+    }
     if (t == 0) S.rot = 0;
     __syncthreads();
+    const int nact = S.nact;
+    const int np = nact + (nact & 1), N = np - 1, npair = np / 2;
+    if (N <= 0) { ++sweep; break; }
     for (int r = 0; r < N; ++r) {
       for (int pi0 = 0; pi0 < npair; pi0 += ngroups) {
         const int pi = pi0 + grp;
         int p = 0, q = n;
-        if (pi < npair) pair_of(r, pi, N, p, q);
+        if (pi < npair) {
+          int pp, qq;
+          pair_of(r, pi, N, pp, qq);
+          if (qq < nact) {
+            p = S.act[pp]; q = S.act[qq];
+            if (p > q) { const int x = p; p = q; q = x; }
+          }
+        }
         const bool act = pi < npair && q < n;
         double a = 0.0, b = 0.0;
         if (act) { a = S.nrm[p]; b = S.nrm[q]; }
