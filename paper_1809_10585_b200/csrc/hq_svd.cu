@@ -86,20 +86,21 @@ __global__ void __launch_bounds__(1024) power_kernel(double* x0, const double* w
 bool g_svd_attr = false;
 }  // namespace
 
-template <int G, int LP>
+template <int G>
 static int launch_cluster(cudaStream_t st, const hq_svd_prob* probs, int nprob, int* rank,
                           const double* scal) {
   static bool attr = false;
-  auto kern = svd_cluster_kernel<G, LP>;
+  auto kern = svd_cluster_kernel<G>;
+  const int smem = (int)(sizeof(CSmem) > sizeof(SvdSmem) ? sizeof(CSmem) : sizeof(SvdSmem));
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CSmem));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return (int)e;
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nprob * G);
   cfg.blockDim = dim3(CNT);
-  cfg.dynamicSmemBytes = sizeof(CSmem);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -111,23 +112,15 @@ static int launch_cluster(cudaStream_t st, const hq_svd_prob* probs, int nprob, 
   return (int)cudaLaunchKernelEx(&cfg, kern, probs, rank, scal);
 }
 
-template <int G>
-static int launch_cluster_lp(cudaStream_t st, const hq_svd_prob* probs, int nprob, int* rank,
-                             const double* scal, int max_m) {
-  if (max_m <= 128) return launch_cluster<G, 8>(st, probs, nprob, rank, scal);
-  if (max_m <= 256) return launch_cluster<G, 16>(st, probs, nprob, rank, scal);
-  return launch_cluster<G, 32>(st, probs, nprob, rank, scal);
-}
-
 extern "C" int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank,
                       const double* scal, int cluster, int max_m) {
   if (nprob <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   if (cluster >= 2) {
     if (max_m > 512) return (int)cudaErrorInvalidValue;
-    if (cluster == 2) return launch_cluster_lp<2>(st, probs, nprob, rank, scal, max_m);
-    if (cluster <= 4) return launch_cluster_lp<4>(st, probs, nprob, rank, scal, max_m);
-    return launch_cluster_lp<8>(st, probs, nprob, rank, scal, max_m);
+    if (cluster == 2) return launch_cluster<2>(st, probs, nprob, rank, scal);
+    if (cluster <= 4) return launch_cluster<4>(st, probs, nprob, rank, scal);
+    return launch_cluster<8>(st, probs, nprob, rank, scal);
   }
   if (!g_svd_attr) {
     cudaError_t e = cudaFuncSetAttribute(svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -1,83 +1,42 @@
 // One-sided block Jacobi on a thread-block cluster (included by hq_svd.cu).
-// For truncation cores too large for one SM's shared memory (m*n > ~24K
-// doubles, i.e. n >~ 155), the n columns of X are split into 2G blocks of bs
-// columns; CTA c of a G-CTA cluster holds two blocks in its shared memory.
-// A sweep = intra-block pairs (round 0) + the 2G-1 rounds of a block
-// round-robin tournament (circle method): each round every CTA rotates all
-// pairs between its two blocks, then the blocks move between CTAs through
-// distributed shared memory (pull into staging buffers, cluster barrier,
-// local copy).  Columns never leave the cluster's SMs until U_k is written.
+// For truncation cores too large for one SM (m*n > ~24K doubles, or more
+// pairs per round than one CTA has lane groups), the n columns of X are split
+// into 2G blocks of bs columns; CTA c of a G-CTA cluster holds two blocks in
+// its shared memory.  A sweep = intra-block pairs (circle method inside both
+// blocks) + the 2G-1 rounds of a block round-robin tournament: each round
+// every CTA rotates all pairs between its two blocks (the slot-0 columns stay
+// in registers for the whole round, only slot-1 columns stream through
+// shared memory), then every CTA pushes its two blocks into the spare buffer
+// set of the CTAs that own their next tournament positions (distributed
+// shared memory stores) and the cluster meets at ONE barrier; buffer sets
+// alternate, so nothing is copied locally.  The convergence flags travel with
+// the last push of a sweep.  Columns never leave the cluster's SMs until U_k
+// is written.
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
+
+#ifndef HQ_SVD_SINGLE_MAX_PAIRS
+#define HQ_SVD_SINGLE_MAX_PAIRS 16
+#endif
 
 namespace {
 constexpr int CNT = 512, CNW = CNT / 32;
 constexpr int C_MAX_BS = 64;          // max columns per block
-constexpr int C_SMEM_DOUBLES = 22528; // 176 KB: 4 block buffers (2 work + 2 staging)
+constexpr int C_SMEM_DOUBLES = 22528; // 176 KB: 2 buffer sets x 2 blocks
 
 struct CSmem {
   double buf[C_SMEM_DOUBLES];
-  double nrm[4][C_MAX_BS];   // carried squared norms of the four block buffers
-  int col[4][C_MAX_BS];      // global column index held in each buffer slot (-1: pad)
+  double nrm[4][C_MAX_BS];   // squared norms, [set * 2 + slot]
+  int col[4][C_MAX_BS];      // global column index per slot (-1: pad)
   double sig_all[1024];
+  int flag[2][8];            // rotation flags of every CTA, by sweep parity
+  double2 trash[32];         // sink for the stores of rows past the column end
   int rot;
-  int done;
   int cnt;
+#ifdef HQ_DEBUG_SWEEPS
+  long long dbg[4];
+#endif
 };
-
-// rotate pair (x, y) of columns held in smem (ld even), group of LP lanes
-template <int LP>
-__device__ __forceinline__ bool rotate_pair(double* cx, double* cy, double& a, double& b, int ld,
-                                            double tol, double tiny2, double thr2, int gl, bool act) {
-  constexpr int E = 16;
-  double xp[E], xq[E];
-  const bool work = act && !(a + b < thr2) && !(a < tiny2 && b < tiny2);
-  double g0 = 0.0, g1 = 0.0;
-#pragma unroll
-  for (int e = 0; e < E / 2; ++e) {
-    const int i = 2 * gl + 2 * LP * e;
-    double2 vp = make_double2(0.0, 0.0), vq = make_double2(0.0, 0.0);
-    if (work && i < ld) {
-      vp = *reinterpret_cast<const double2*>(cx + i);
-      vq = *reinterpret_cast<const double2*>(cy + i);
-    }
-    xp[2 * e] = vp.x; xp[2 * e + 1] = vp.y;
-    xq[2 * e] = vq.x; xq[2 * e + 1] = vq.y;
-    g0 = fma(vp.x, vq.x, g0);
-    g1 = fma(vp.y, vq.y, g1);
-  }
-  double g = g0 + g1;
-#pragma unroll
-  for (int o = LP / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
-  const bool rot = work && g != 0.0 && g * g > (tol * tol) * (a * b);
-  if (rot) {
-    // zeta = (b - a) / 2g in single precision on exponent-normalized operands
-    int eg;
-    frexp(g, &eg);
-    const double num = ldexp(b - a, -eg), den = ldexp(2.0 * g, -eg);   // |den| in [1, 2)
-    double tt;
-    if (fabs(num) < 1e18) {
-      const float zf = __fdividef((float)num, (float)den);
-      tt = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
-    } else {
-      tt = 0.5 * den / num;
-    }
-    const double c = rsqrt(1.0 + tt * tt), sn = c * tt;
-#pragma unroll
-    for (int e = 0; e < E / 2; ++e) {
-      const int i = 2 * gl + 2 * LP * e;
-      if (i < ld) {
-        *reinterpret_cast<double2*>(cx + i) =
-            make_double2(c * xp[2 * e] - sn * xq[2 * e], c * xp[2 * e + 1] - sn * xq[2 * e + 1]);
-        *reinterpret_cast<double2*>(cy + i) =
-            make_double2(sn * xp[2 * e] + c * xq[2 * e], sn * xp[2 * e + 1] + c * xq[2 * e + 1]);
-      }
-    }
-    a = fmax(a - tt * g, 0.0);
-    b = b + tt * g;
-  }
-  return rot;
-}
 
 // block owner map of the circle tournament: position -> (cta, slot)
 // top row: positions 0..G-1 are slot 0 of CTA c; bottom row: slot 1 of CTA
@@ -89,46 +48,23 @@ __device__ __forceinline__ int circ_next(int pos, int G) {
   return pos == P - 1 ? 1 : pos + 1;
 }
 
-template <int G, int LP>
-__global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* __restrict__ probs,
-                                                             int* __restrict__ rank,
-                                                             const double* __restrict__ scal) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  CSmem& S = *reinterpret_cast<CSmem*>(smem_raw);
-  cg::cluster_group cluster = cg::this_cluster();
+template <int G, int LP, int E>
+__device__ __noinline__ void svd_cluster_body(const hq_svd_prob& P, int* __restrict__ rank, int m, int n,
+                                                 double thr, CSmem& S, cg::cluster_group& cluster) {
   const int cr = (int)cluster.block_rank();
-  const hq_svd_prob P = probs[blockIdx.x / G];
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   constexpr int GPW = 32 / LP;
   const int grp = wid * GPW + lane / LP, gl = lane % LP, ngroups = CNW * GPW;
-  const int m = hq_dim(rank, P.m, P.m_ri);
-  int n = hq_dim(rank, P.n, P.n_ri);
-  if (P.xform) n = min(n, m);
-  n = min(n, 1024);
-  const double thr = P.eps_scale * (P.eps_slot >= 0 ? scal[P.eps_slot] : 1.0);
-  if (m <= 0 || n <= 0) {
-    if (cr == 0 && t == 0) rank[P.rank_ri] = 0;
-    return;
-  }
   const int ld = (m + 1) & ~1;
   const int bs = (n + 2 * G - 1) / (2 * G);
-  if (4 * bs * ld > C_SMEM_DOUBLES || bs > C_MAX_BS || G * 2 * bs > 1024) {
-    // the plan picked a cluster too small for this run-time size
-    if (cr == 0 && t == 0) {
-      if (P.flag_ri >= 0) rank[P.flag_ri] = 1;
-      rank[P.rank_ri] = 0;
-    }
-    return;
-  }
-  // buffers: 0,1 = working slots; 2,3 = staging
-  double* B[4];
-  for (int k = 0; k < 4; ++k) B[k] = S.buf + (size_t)k * bs * ld;
-  // ---- initial load: CTA cr holds positions cr (slot 0) and 2G-1-cr (slot 1)
+  // buffer set k: blocks Bk(slot) = buf + (2k + slot) bs ld; sets alternate per exchange
+  auto blk = [&](int set, int slot) { return S.buf + (size_t)(2 * set + slot) * bs * ld; };
+  // ---- initial load into set 0: CTA cr holds positions cr (slot 0) and 2G-1-cr (slot 1)
   for (int slot = 0; slot < 2; ++slot) {
     const int pos = slot == 0 ? cr : 2 * G - 1 - cr;
     for (int jj = 0; jj < bs; ++jj) {
       const int j = pos * bs + jj;
-      double* dst = B[slot] + (size_t)jj * ld;
+      double* dst = blk(0, slot) + (size_t)jj * ld;
       for (int i = t; i < ld; i += CNT) {
         double v = 0.0;
         if (j < n && i < m) v = P.xform ? (j <= i ? P.c[j + (size_t)i * P.ldc] : 0.0)
@@ -138,110 +74,198 @@ __global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* 
       if (t == 0) S.col[slot][jj] = j < n ? j : -1;
     }
   }
-  __syncthreads();
+  // destination (cta, slot) of my two blocks after each tournament round
+  int dcta[2], dslot[2];
+  for (int slot = 0; slot < 2; ++slot) {
+    const int np = circ_next(slot == 0 ? cr : 2 * G - 1 - cr, G);
+    dcta[slot] = np < G ? np : 2 * G - 1 - np;
+    dslot[slot] = np < G ? 0 : 1;
+  }
+  cluster.sync();
   const double tol = 4.0 * sqrt((double)m) * 2.220446049250313e-16;
-  const double tiny2 = (1e-3 * thr) * (1e-3 * thr), thr2 = thr * thr;
+  const double tiny2 = (1e-3 * thr) * (1e-3 * thr), thr2 = thr * thr, tol2 = tol * tol;
+  const bool reg_x = bs <= ngroups;   // one pass of groups per round: slot-0 column in registers
+  int cur = 0;
+#ifdef HQ_DEBUG_SWEEPS
+  if (t < 4) S.dbg[t] = 0;
+  long long dbg_t[4] = {0, 0, 0, 0};
+  long long dbg_c = clock64();
+#define HQ_DBG_MARK(k) do { const long long c_ = clock64(); dbg_t[k] += c_ - dbg_c; dbg_c = c_; } while (0)
+#else
+#define HQ_DBG_MARK(k) do { } while (0)
+#endif
+  int nsw = 0;
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
+    nsw = sweep + 1;
+    double* B0 = blk(cur, 0);
+    double* B1 = blk(cur, 1);
+    double* nrm0 = S.nrm[2 * cur];
+    double* nrm1 = S.nrm[2 * cur + 1];
+    const int* col0 = S.col[2 * cur];
+    const int* col1 = S.col[2 * cur + 1];
     // squared norms of the two working blocks
     for (int j = wid; j < 2 * bs; j += CNW) {
-      const double* x = B[j / bs] + (size_t)(j % bs) * ld;
+      const double* x = (j < bs ? B0 : B1) + (size_t)(j % bs) * ld;
       double v = 0.0;
       for (int i = lane; i < ld; i += 32) v = fma(x[i], x[i], v);
       v = warp_sum(v);
-      if (lane == 0) S.nrm[j / bs][j % bs] = v;
+      if (lane == 0) (j < bs ? nrm0 : nrm1)[j % bs] = v;
     }
     if (t == 0) S.rot = 0;
     __syncthreads();
+    HQ_DBG_MARK(0);
     // intra-block pairs of both working blocks (round robin inside each block)
     {
-      const int npb = bs + (bs & 1), N = npb - 1;
+      const int npb = bs + (bs & 1), N = npb - 1, hp = npb / 2;
       for (int r = 0; r < N; ++r) {
-        for (int g0 = 0; g0 < 2 * (npb / 2); g0 += ngroups) {
+        for (int g0 = 0; g0 < 2 * hp; g0 += ngroups) {
+          if (g0 + wid * GPW >= 2 * hp) break;  // warp-uniform
           const int gi = g0 + grp;
-          const int blk = gi / (npb / 2), pi = gi % (npb / 2);
+          const int bk = gi >= hp ? 1 : 0, pi = gi - bk * hp;
+          const int* colb = bk ? col1 : col0;
+          double* nrmb = bk ? nrm1 : nrm0;
           int p = 0, q = 0;
-          bool act = gi < 2 * (npb / 2);
+          bool act = gi < 2 * hp;
           if (act) {
-            pair_of(r, pi, N, p, q);
-            act = q < bs && S.col[blk][p] >= 0 && S.col[blk][q] >= 0;
+            p = r; q = N;
+            if (pi != 0) {
+              p = r + pi; if (p >= N) p -= N;
+              q = r - pi; if (q < 0) q += N;
+            }
+            if (p > q) { const int x = p; p = q; q = x; }
+            act = q < bs && colb[p] >= 0 && colb[q] >= 0;
           }
-          double a = act ? S.nrm[blk][p] : 0.0, b = act ? S.nrm[blk][q] : 0.0;
-          const bool rr = rotate_pair<LP>(B[blk & 1] + (size_t)p * ld, B[blk & 1] + (size_t)q * ld, a, b,
-                                          ld, tol, tiny2, thr2, gl, act);
-          if (rr && gl == 0) { S.nrm[blk][p] = a; S.nrm[blk][q] = b; S.rot = 1; }
+          if (!act) { p = 0; q = 0; }
+          double a = act ? nrmb[p] : 0.0, b = act ? nrmb[q] : 0.0;
+          double* Bb = bk ? B1 : B0;
+          double xp[E];
+          const bool rr = jacobi_pair<LP, E, false>(xp, Bb + (size_t)p * ld, Bb + (size_t)q * ld, a, b, ld, tol2,
+                                                    tiny2, thr2, gl, act, S.trash);
+          if (rr && gl == 0) { nrmb[p] = a; nrmb[q] = b; S.rot = 1; }
         }
         __syncthreads();
       }
     }
-    // 2G-1 tournament rounds of inter-block pairs
+    HQ_DBG_MARK(1);
+    // 2G-1 tournament rounds of inter-block pairs, each followed by a push
     for (int round = 0; round < 2 * G - 1; ++round) {
-      for (int r = 0; r < bs; ++r) {
-        for (int g0 = 0; g0 < bs; g0 += ngroups) {
-          const int i = g0 + grp;
-          const int j = (i + r) % bs;
-          bool act = i < bs && S.col[0][i] >= 0 && S.col[1][j] >= 0;
-          double a = act ? S.nrm[0][i] : 0.0, b = act ? S.nrm[1][j] : 0.0;
-          const bool rr = rotate_pair<LP>(B[0] + (size_t)i * ld, B[1] + (size_t)j * ld, a, b, ld, tol, tiny2,
-                                          thr2, gl, act);
-          if (rr && gl == 0) { S.nrm[0][i] = a; S.nrm[1][j] = b; S.rot = 1; }
+      if (reg_x) {
+        const int i = grp;
+        const bool own = i < bs && col0[i] >= 0;
+        double xp[E];
+        double a = own ? nrm0[i] : 0.0;
+#pragma unroll
+        for (int e = 0; e < E / 2; ++e) {
+          const int ii = 2 * gl + 2 * LP * e;
+          double2 v = make_double2(0.0, 0.0);
+          if (own && ii < ld) v = *reinterpret_cast<const double2*>(B0 + (size_t)i * ld + ii);
+          xp[2 * e] = v.x; xp[2 * e + 1] = v.y;
         }
-        __syncthreads();
-      }
-      if (round == 2 * G - 2) break;
-      // move blocks: the block at position p goes to circ_next(p); pull the
-      // blocks that land in my two slots from their current owners
-      cluster.sync();
-      for (int slot = 0; slot < 2; ++slot) {
-        const int mypos = slot == 0 ? cr : 2 * G - 1 - cr;
-        // source position: the one whose circ_next == mypos
-        int src = mypos;
-        for (int p = 0; p < 2 * G; ++p)
-          if (circ_next(p, G) == mypos) { src = p; break; }
-        const int scta = src < G ? src : 2 * G - 1 - src;
-        const int sslot = src < G ? 0 : 1;
-        CSmem* R = cluster.map_shared_rank(&S, scta);
-        const double* sb = R->buf + (size_t)sslot * bs * ld;
-        double* db = B[2 + slot];
-        for (int e = t; e < bs * ld; e += CNT) db[e] = sb[e];
-        for (int jj = t; jj < bs; jj += CNT) {
-          S.nrm[2 + slot][jj] = R->nrm[sslot][jj];
-          S.col[2 + slot][jj] = R->col[sslot][jj];
+        bool any = false;
+        for (int r = 0; r < bs; ++r) {
+#ifdef HQ_DEBUG_SWEEPS
+          const long long q0 = clock64();
+#endif
+          if (wid * GPW < bs) {  // warp-uniform
+            int j = i + r; if (j >= bs) j -= bs;
+            if (!own) j = 0;
+            const bool act = own && col1[j] >= 0;
+            double b = act ? nrm1[j] : 0.0;
+            const bool rr = jacobi_pair<LP, E, true>(xp, B0, B1 + (size_t)j * ld, a, b, ld, tol2, tiny2, thr2, gl,
+                                                     act, S.trash);
+            if (rr && gl == 0) nrm1[j] = b;
+            any |= rr;
+          }
+#ifdef HQ_DEBUG_SWEEPS
+          const long long q1 = clock64();
+#endif
+          __syncthreads();
+#ifdef HQ_DEBUG_SWEEPS
+          if (t == 0) { S.dbg[0] += q1 - q0; S.dbg[1] += clock64() - q1; S.dbg[2] += 1; }
+#endif
         }
-      }
-      cluster.sync();
-      for (int e = t; e < 2 * bs * ld; e += CNT) B[0][e] = B[2][e];   // buffers 0,1 contiguous
-      for (int jj = t; jj < 2 * bs; jj += CNT) {
-        S.nrm[jj / bs][jj % bs] = S.nrm[2 + jj / bs][jj % bs];
-        S.col[jj / bs][jj % bs] = S.col[2 + jj / bs][jj % bs];
+        if (own) {
+#pragma unroll
+          for (int e = 0; e < E / 2; ++e) {
+            const int ii = 2 * gl + 2 * LP * e;
+            if (ii < ld)
+              *reinterpret_cast<double2*>(B0 + (size_t)i * ld + ii) = make_double2(xp[2 * e], xp[2 * e + 1]);
+          }
+          if (gl == 0) { nrm0[i] = a; if (any) S.rot = 1; }
+        }
+      } else {
+        for (int r = 0; r < bs; ++r) {
+          for (int g0 = 0; g0 < bs; g0 += ngroups) {
+            if (g0 + wid * GPW >= bs) break;  // warp-uniform
+            const int i = g0 + grp;
+            int j = i + r; if (j >= bs) j -= bs;
+            bool act = i < bs && col0[i] >= 0 && col1[j] >= 0;
+            double a = act ? nrm0[i] : 0.0, b = act ? nrm1[j] : 0.0;
+            double xp[E];
+            const bool rr = jacobi_pair<LP, E, false>(xp, B0 + (size_t)(act ? i : 0) * ld,
+                                                      B1 + (size_t)(act ? j : 0) * ld, a, b, ld, tol2, tiny2, thr2,
+                                                      gl, act, S.trash);
+            if (rr && gl == 0) { nrm0[i] = a; nrm1[j] = b; S.rot = 1; }
+          }
+          __syncthreads();
+        }
       }
       __syncthreads();
+      HQ_DBG_MARK(2);
+      // push both blocks (and their norms / column ids) to the next owners' spare set
+      const int nxt = cur ^ 1;
+      for (int slot = 0; slot < 2; ++slot) {
+        CSmem* R = cluster.map_shared_rank(&S, dcta[slot]);
+        const double2* src = reinterpret_cast<const double2*>(blk(cur, slot));
+        double2* dst = reinterpret_cast<double2*>(R->buf + (size_t)(2 * nxt + dslot[slot]) * bs * ld);
+        for (int e = t; e < bs * ld / 2; e += CNT) dst[e] = src[e];
+        for (int jj = t; jj < bs; jj += CNT) {
+          R->nrm[2 * nxt + dslot[slot]][jj] = S.nrm[2 * cur + slot][jj];
+          R->col[2 * nxt + dslot[slot]][jj] = S.col[2 * cur + slot][jj];
+        }
+      }
+      if (round == 2 * G - 2 && t < G) cluster.map_shared_rank(&S, t)->flag[sweep & 1][cr] = S.rot;
+      cluster.sync();
+      HQ_DBG_MARK(3);
+      cur = nxt;
+      B0 = blk(cur, 0); B1 = blk(cur, 1);
+      nrm0 = S.nrm[2 * cur]; nrm1 = S.nrm[2 * cur + 1];
+      col0 = S.col[2 * cur]; col1 = S.col[2 * cur + 1];
     }
-    // cluster-wide convergence test
-    cluster.sync();
-    if (t == 0) {
-      int any = 0;
-      for (int c = 0; c < G; ++c) any |= cluster.map_shared_rank(&S, c)->rot;
-      S.done = any ? 0 : 1;
-    }
-    cluster.sync();
-    if (S.done) break;
-    // the blocks are now at shifted positions; restart the tournament from
+    int any = 0;
+#pragma unroll
+    for (int c = 0; c < G; ++c) any |= S.flag[sweep & 1][c];
+    if (!any) break;
+    // the blocks are now at shifted positions; the next sweep starts from
     // the current placement (any placement is a valid starting position)
   }
+#ifdef HQ_DEBUG_SWEEPS
+  if (cr == 0 && t == 0 && P.flag_ri >= 0) {
+    rank[P.flag_ri + 1] = nsw;
+    for (int k = 0; k < 4; ++k) rank[P.flag_ri + 2 + k] = (int)(dbg_t[k] >> 4);
+    rank[P.flag_ri + 6] = (int)(S.dbg[0] / max(1LL, S.dbg[2]));
+    rank[P.flag_ri + 7] = (int)(S.dbg[1] / max(1LL, S.dbg[2]));
+  }
+#endif
+#undef HQ_DBG_MARK
+  (void)nsw;
+  double* Bs[2] = {blk(cur, 0), blk(cur, 1)};
+  double* nrms[2] = {S.nrm[2 * cur], S.nrm[2 * cur + 1]};
+  const int* cols[2] = {S.col[2 * cur], S.col[2 * cur + 1]};
   // ---- singular values, global order, output U_k
   for (int j = wid; j < 2 * bs; j += CNW) {
-    const double* x = B[j / bs] + (size_t)(j % bs) * ld;
+    const double* x = Bs[j / bs] + (size_t)(j % bs) * ld;
     double v = 0.0;
     for (int i = lane; i < ld; i += 32) v = fma(x[i], x[i], v);
     v = sqrt(warp_sum(v));
-    if (lane == 0) S.nrm[j / bs][j % bs] = S.col[j / bs][j % bs] >= 0 ? v : -1.0;
+    if (lane == 0) nrms[j / bs][j % bs] = cols[j / bs][j % bs] >= 0 ? v : -1.0;
   }
   cluster.sync();
-  // gather (column id, sigma) of every slot of every CTA
+  // gather sigma of every slot of every CTA
   for (int e = t; e < G * 2 * bs; e += CNT) {
     const int c = e / (2 * bs), k = e % (2 * bs);
     CSmem* R = cluster.map_shared_rank(&S, c);
-    S.sig_all[e] = R->nrm[k / bs][k % bs];
+    S.sig_all[e] = R->nrm[2 * cur + k / bs][k % bs];
   }
   if (t == 0) S.cnt = 0;
   cluster.sync();
@@ -260,7 +284,7 @@ __global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* 
     if (lane == 0) atomicAdd(&S.cnt, 1);
     if (pos < P.cap) {
       const double inv = 1.0 / sj;
-      const double* x = B[k / bs] + (size_t)(k % bs) * ld;
+      const double* x = Bs[k / bs] + (size_t)(k % bs) * ld;
       for (int i = lane; i < m; i += 32) P.u[i + (size_t)pos * P.ldu] = x[i] * inv;
     }
   }
@@ -272,5 +296,53 @@ __global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* 
     rank[P.rank_ri] = kk;
   }
   cluster.sync();
+}
+
+template <int G>
+__global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* __restrict__ probs,
+                                                             int* __restrict__ rank,
+                                                             const double* __restrict__ scal) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cr = (int)cluster.block_rank();
+  const hq_svd_prob P = probs[blockIdx.x / G];
+  const int t = threadIdx.x;
+  const int m = hq_dim(rank, P.m, P.m_ri);
+  int n = hq_dim(rank, P.n, P.n_ri);
+  if (P.xform) n = min(n, m);
+  n = min(n, 1024);
+  const double thr = P.eps_scale * (P.eps_slot >= 0 ? scal[P.eps_slot] : 1.0);
+  if (m <= 0 || n <= 0) {
+    if (cr == 0 && t == 0) rank[P.rank_ri] = 0;
+    return;
+  }
+  // the plan sizes clusters from capacities; a core that fits one SM with one
+  // pass of pairs per round runs on CTA 0 alone (no exchange rounds)
+  // the plan sizes clusters from capacities; the run-time core decides: one
+  // SM when it fits with few pairs per round (no exchange rounds), the
+  // cluster when its blocks fit the cluster's shared memory, else CTA 0 alone
+  // on the global-memory path
+  const int ld = (m + 1) & ~1;
+  const int bs = (n + 2 * G - 1) / (2 * G);
+  const bool fits_single = (size_t)ld * n <= SMEM_DOUBLES;
+  const bool fits_cluster = m <= 512 && 4 * bs * ld <= C_SMEM_DOUBLES && bs <= C_MAX_BS;
+  if (!fits_cluster || (fits_single && (n + 1) / 2 <= HQ_SVD_SINGLE_MAX_PAIRS)) {
+    if (cr == 0) svd_single(P, rank, scal, *reinterpret_cast<SvdSmem*>(smem_raw));
+    return;
+  }
+  CSmem& S = *reinterpret_cast<CSmem*>(smem_raw);
+  // lane-group shape from the pairs per CTA (bs) and the rows (m)
+  if (bs <= 16 || m > 256) {
+    if (m <= 128) svd_cluster_body<G, 32, 4>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 256) svd_cluster_body<G, 32, 8>(P, rank, m, n, thr, S, cluster);
+    else svd_cluster_body<G, 32, 16>(P, rank, m, n, thr, S, cluster);
+  } else if (bs <= 32 || m > 128) {
+    if (m <= 128) svd_cluster_body<G, 16, 8>(P, rank, m, n, thr, S, cluster);
+    else svd_cluster_body<G, 16, 16>(P, rank, m, n, thr, S, cluster);
+  } else {
+    if (m <= 64) svd_cluster_body<G, 8, 8>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 128) svd_cluster_body<G, 8, 16>(P, rank, m, n, thr, S, cluster);
+    else svd_cluster_body<G, 16, 16>(P, rank, m, n, thr, S, cluster);
+  }
 }
 }  // namespace

@@ -18,6 +18,7 @@ struct SvdSmem {
   double rc[MAX_N / 2];
   double rs[MAX_N / 2];
   double rt[MAX_N / 2];
+  double2 trash[32];  // sink for the stores of rows past the column end
   int rot;
   int cnt;
 };
@@ -28,11 +29,119 @@ __device__ __forceinline__ void pair_of(int r, int pi, int N, int& p, int& q) {
   if (p > q) { const int x = p; p = q; q = x; }
 }
 
+__device__ __forceinline__ double rcp_approx(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+__device__ __forceinline__ double rsqrt_approx(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
+// Tangent t of the Jacobi rotation for the pair with squared norms a, b and
+// inner product g (g != 0): t = sign(z) / (|z| + sqrt(1 + z^2)), z = (b-a)/2g.
+// Any t gives an exactly orthogonal rotation once c = (1+t^2)^(-1/2) is
+// accurate, so t is formed from the hardware reciprocal / reciprocal-sqrt
+// approximations (~2^-22 relative: at most one extra sweep); only c is
+// computed to full FP64 accuracy by the caller.
+__device__ __forceinline__ double jacobi_tan(double a, double b, double g) {
+  const double d = b - a;
+  const double h = fabs(d) * (0.5 * rcp_approx(fabs(g)));
+  const double w = fma(h, h, 1.0);
+  const double t = h < 1e150 ? rcp_approx(fma(w, rsqrt_approx(w), h)) : 0.5 * rcp_approx(h);
+  return ((d >= 0.0) == (g > 0.0)) ? t : -t;
+}
+
+// One pair update by a group of LP lanes; lane gl owns rows 2gl + 2LP e + {0,1}
+// (e < E/2) of both columns, so a group moves 16 B x LP contiguous bytes per
+// access (conflict-free 128-bit shared memory traffic).  XREG: column x lives
+// in the registers xp across calls (only y streams through shared memory).
+// Rows past the column end read row 0 (masked) and store into a sink, so the
+// body is branch-free apart from the rotation itself.
+template <int LP, int E, bool XREG>
+__device__ __forceinline__ bool jacobi_pair(double (&xp)[E], double* cx, double* cy, double& a, double& b,
+                                            int ld, double tol2, double tiny2, double thr2, int gl, bool act,
+                                            double2* trash) {
+  const bool work = act && !(a + b < thr2) && !(a < tiny2 && b < tiny2);
+  double xq[E];
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+#pragma unroll
+  for (int e = 0; e < E / 2; ++e) {
+    const int i = 2 * gl + 2 * LP * e;
+    const bool in = work && i < ld;
+    const int ii = in ? i : 0;
+    const double2 vq = *reinterpret_cast<const double2*>(cy + ii);
+    if (!XREG) {
+      const double2 vp = *reinterpret_cast<const double2*>(cx + ii);
+      xp[2 * e] = in ? vp.x : 0.0;
+      xp[2 * e + 1] = in ? vp.y : 0.0;
+    }
+    xq[2 * e] = in ? vq.x : 0.0;
+    xq[2 * e + 1] = in ? vq.y : 0.0;
+    if (e & 1) {
+      g2 = fma(xp[2 * e], xq[2 * e], g2);
+      g3 = fma(xp[2 * e + 1], xq[2 * e + 1], g3);
+    } else {
+      g0 = fma(xp[2 * e], xq[2 * e], g0);
+      g1 = fma(xp[2 * e + 1], xq[2 * e + 1], g1);
+    }
+  }
+  double g = (g0 + g1) + (g2 + g3);
+#pragma unroll
+  for (int o = LP / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+  const bool rot = work && g != 0.0 && g * g > tol2 * (a * b);
+  if (rot) {
+    const double tt = jacobi_tan(a, b, g);
+    const double c = rsqrt(fma(tt, tt, 1.0)), sn = c * tt;
+    double2* sink = trash + (threadIdx.x & 31);
+#pragma unroll
+    for (int e = 0; e < E / 2; ++e) {
+      const int i = 2 * gl + 2 * LP * e;
+      const double x0 = xp[2 * e], x1 = xp[2 * e + 1], y0 = xq[2 * e], y1 = xq[2 * e + 1];
+      const double2 nx = make_double2(c * x0 - sn * y0, c * x1 - sn * y1);
+      const double2 ny = make_double2(sn * x0 + c * y0, sn * x1 + c * y1);
+      if (XREG) {
+        xp[2 * e] = nx.x;
+        xp[2 * e + 1] = nx.y;
+      } else {
+        *(i < ld ? reinterpret_cast<double2*>(cx + i) : sink) = nx;
+      }
+      *(i < ld ? reinterpret_cast<double2*>(cy + i) : sink) = ny;
+    }
+    a = fmax(a - tt * g, 0.0);
+    b = b + tt * g;
+  }
+  return rot;
+}
+
+// Stable compaction of the active column list (warp 0): columns whose squared
+// norm fell below tiny2 leave the rotation set.
+__device__ __forceinline__ void compact_active(short* act, int& nact_out, const double* nrm, int nact,
+                                               double tiny2) {
+  const int lane = threadIdx.x & 31;
+  int k = 0;
+  for (int j0 = 0; j0 < nact; j0 += 32) {
+    const int jj = j0 + lane;
+    const int j = jj < nact ? act[jj] : 0;
+    const bool keep = jj < nact && !(nrm[j] < tiny2);
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    __syncwarp();
+    if (keep) act[k + __popc(bal & ((1u << lane) - 1u))] = (short)j;
+    k += __popc(bal);
+    __syncwarp();
+  }
+  if (lane == 0) nact_out = k;
+}
+
 // One-sided Jacobi with each pair owned by a group of LP lanes holding both
-// columns in registers (E = m / LP <= 16 doubles per lane per column): one
-// smem read and one smem write of each column per round, dot product reduced
-// with log2(LP) shuffles, the rotation parameters computed by the group.
-template <int LP, bool SMEM, int E = 16>
+// columns in registers (E = rows per lane per column): one smem read and one
+// smem write of each column per round, dot product reduced with log2(LP)
+// shuffles, the rotation parameters computed by the group.  Warps without a
+// pair in a round skip straight to the barrier (they would otherwise steal
+// issue slots from the latency-bound active warps).
+template <int LP, bool SMEM, int E>
 __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, double tiny2, double thr,
                              SvdSmem& S) {
   // SMEM: index the staged copy through S.cs so the compiler emits LDS/STS
@@ -41,6 +150,7 @@ __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, doubl
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int grp = wid * GPW + lane / LP, gl = lane % LP;
   const int ngroups = NW * GPW;
+  const double tol2 = tol * tol, thr2 = thr * thr;
   for (int j = t; j < n; j += NT) S.act[j] = (short)j;
   if (t == 0) S.nact = n;
   __syncthreads();
@@ -59,98 +169,68 @@ __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, doubl
     // after the first sweep, columns far below the threshold (norm < 1e-3 thr)
     // leave the rotation set: they are dropped by the truncation and moving
     // them changes the kept columns by less than that
-    if (sweep >= 1 && t == 0) {
-      int k = 0;
-      for (int jj = 0; jj < nact0; ++jj) {
-        const int j = S.act[jj];
-        if (!(S.nrm[j] < tiny2)) S.act[k++] = (short)j;
-      }
-      S.nact = k;
-    }
+    if (sweep >= 1 && wid == 0) compact_active(S.act, S.nact, S.nrm, nact0, tiny2);
     if (t == 0) S.rot = 0;
     __syncthreads();
     const int nact = S.nact;
-    const int np = nact + (nact & 1), N = np - 1, npair = np / 2;
+    const int npair = (nact + 1) / 2, N = 2 * npair - 1;
     if (N <= 0) { ++sweep; break; }
     for (int r = 0; r < N; ++r) {
       for (int pi0 = 0; pi0 < npair; pi0 += ngroups) {
+        if (pi0 + wid * GPW >= npair) break;  // warp-uniform
         const int pi = pi0 + grp;
         int p = 0, q = n;
         if (pi < npair) {
-          int pp, qq;
-          pair_of(r, pi, N, pp, qq);
-          if (qq < nact) {
+          // round-robin (circle) pair pi of round r
+          int pp = r, qq = N;
+          if (pi != 0) {
+            pp = r + pi; if (pp >= N) pp -= N;
+            qq = r - pi; if (qq < 0) qq += N;
+          }
+          if (pp < nact && qq < nact) {
             p = S.act[pp]; q = S.act[qq];
             if (p > q) { const int x = p; p = q; q = x; }
           }
         }
-        const bool act = pi < npair && q < n;
+        const bool act = q < n;
         double a = 0.0, b = 0.0;
         if (act) { a = S.nrm[p]; b = S.nrm[q]; }
-        const bool work = act && !(a + b < thr * thr) && !(a < tiny2 && b < tiny2);
-        double xp[E], xq[E];
-        double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
-        double* cp = X + (size_t)p * ld;
-        double* cq = X + (size_t)(work ? q : p) * ld;
         if (SMEM) {
-          // lane gl owns rows 2gl + 2LP e + {0,1}: a group reads 16 B x LP
-          // contiguous bytes per load -> conflict-free 128-bit shared loads
-#pragma unroll
-          for (int e = 0; e < E / 2; ++e) {
-            const int i = 2 * gl + 2 * LP * e;
-            double2 vp = make_double2(0.0, 0.0), vq = make_double2(0.0, 0.0);
-            if (work && i < ld) {
-              vp = *reinterpret_cast<const double2*>(cp + i);
-              vq = *reinterpret_cast<const double2*>(cq + i);
-            }
-            xp[2 * e] = vp.x; xp[2 * e + 1] = vp.y;
-            xq[2 * e] = vq.x; xq[2 * e + 1] = vq.y;
+          double xp[E];
+          double* cp = X + (size_t)p * ld;
+          const bool rr = jacobi_pair<LP, E, false>(xp, cp, act ? X + (size_t)q * ld : cp, a, b, ld, tol2, tiny2,
+                                                    thr2, gl, act, S.trash);
+          if (rr && gl == 0) {
+            S.nrm[p] = a;
+            S.nrm[q] = b;
+            S.rot = 1;
           }
         } else {
+          const bool work = act && !(a + b < thr2) && !(a < tiny2 && b < tiny2);
+          double xp[E], xq[E];
+          double g0 = 0.0, g1 = 0.0, g2 = 0.0, g3 = 0.0;
+          double* cp = X + (size_t)p * ld;
+          double* cq = X + (size_t)(work ? q : p) * ld;
 #pragma unroll
           for (int e = 0; e < E; ++e) {
             const int i = gl + e * LP;
             xp[e] = (work && i < m) ? cp[i] : 0.0;
             xq[e] = (work && i < m) ? cq[i] : 0.0;
           }
-        }
 #pragma unroll
-        for (int e = 0; e < E; e += 4) {
-          g0 = fma(xp[e], xq[e], g0);
-          g1 = fma(xp[e + 1], xq[e + 1], g1);
-          g2 = fma(xp[e + 2], xq[e + 2], g2);
-          g3 = fma(xp[e + 3], xq[e + 3], g3);
-        }
-        double g = (g0 + g1) + (g2 + g3);
-#pragma unroll
-        for (int o = LP / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
-        bool rot = work && g != 0.0 && g * g > (tol * tol) * (a * b);
-        double c = 1.0, sn = 0.0, tt = 0.0;
-        if (rot) {
-          // tangent of the rotation angle: any t gives an exactly orthogonal
-          // rotation once c = (1+t^2)^(-1/2) is accurate, so t is formed in
-          // single precision when in range (costs at most one extra sweep)
-          const double zeta = (b - a) / (2.0 * g);
-          if (fabs(zeta) < 1e18) {
-            const float zf = (float)zeta;
-            tt = (double)(copysignf(1.0f, zf) / (fabsf(zf) + sqrtf(fmaf(zf, zf, 1.0f))));
-          } else {
-            tt = 0.5 / zeta;
+          for (int e = 0; e < E; e += 4) {
+            g0 = fma(xp[e], xq[e], g0);
+            g1 = fma(xp[e + 1], xq[e + 1], g1);
+            g2 = fma(xp[e + 2], xq[e + 2], g2);
+            g3 = fma(xp[e + 3], xq[e + 3], g3);
           }
-          c = rsqrt(1.0 + tt * tt);
-          sn = c * tt;
-          if (SMEM) {
+          double g = (g0 + g1) + (g2 + g3);
 #pragma unroll
-            for (int e = 0; e < E / 2; ++e) {
-              const int i = 2 * gl + 2 * LP * e;
-              if (i < ld) {
-                *reinterpret_cast<double2*>(cp + i) =
-                    make_double2(c * xp[2 * e] - sn * xq[2 * e], c * xp[2 * e + 1] - sn * xq[2 * e + 1]);
-                *reinterpret_cast<double2*>(cq + i) =
-                    make_double2(sn * xp[2 * e] + c * xq[2 * e], sn * xp[2 * e + 1] + c * xq[2 * e + 1]);
-              }
-            }
-          } else {
+          for (int o = LP / 2; o > 0; o >>= 1) g += __shfl_xor_sync(0xffffffffu, g, o);
+          const bool rot = work && g != 0.0 && g * g > tol2 * (a * b);
+          if (rot) {
+            const double tt = jacobi_tan(a, b, g);
+            const double c = rsqrt(fma(tt, tt, 1.0)), sn = c * tt;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
               const int i = gl + e * LP;
@@ -160,11 +240,11 @@ __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, doubl
                 cq[i] = sn * x + c * y;
               }
             }
-          }
-          if (gl == 0) {
-            S.nrm[p] = fmax(a - tt * g, 0.0);
-            S.nrm[q] = b + tt * g;
-            S.rot = 1;
+            if (gl == 0) {
+              S.nrm[p] = fmax(a - tt * g, 0.0);
+              S.nrm[q] = b + tt * g;
+              S.rot = 1;
+            }
           }
         }
       }
@@ -176,12 +256,10 @@ __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, doubl
   return sweep;
 }
 
-__global__ void __launch_bounds__(NT, 1) svd_kernel(const hq_svd_prob* __restrict__ probs,
-                                                    int* __restrict__ rank,
-                                                    const double* __restrict__ scal) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SvdSmem& S = *reinterpret_cast<SvdSmem*>(smem_raw);
-  const hq_svd_prob P = probs[blockIdx.x];
+
+__device__ __noinline__ void svd_single(const hq_svd_prob& Pin, int* __restrict__ rank,
+                                        const double* __restrict__ scal, SvdSmem& S) {
+  const hq_svd_prob P = Pin;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int m = hq_dim(rank, P.m, P.m_ri);
   int n = hq_dim(rank, P.n, P.n_ri);
@@ -220,14 +298,25 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const hq_svd_prob* __restric
   if (m <= 512) {
     // register-cached path: a group of LP lanes owns a pair (E <= 16 rows per lane)
     if (staged) {
-      if (m <= 128) nsweeps = jacobi_groups<8, true>(X, ld, m, n, tol, tiny2, thr, S);
-      else if (m <= 192) nsweeps = jacobi_groups<8, true, 24>(X, ld, m, n, tol, tiny2, thr, S);
-      else if (m <= 256) nsweeps = jacobi_groups<16, true>(X, ld, m, n, tol, tiny2, thr, S);
-      else nsweeps = jacobi_groups<32, true>(X, ld, m, n, tol, tiny2, thr, S);
+      // lane-group shape: as many lanes per pair as one pass of groups allows
+      // (shorter per-pair dependency chains), enough rows per lane for m
+      const int np0 = (n + 1) / 2;
+      if (np0 <= 16 || m > 256) {
+        if (m <= 128) nsweeps = jacobi_groups<32, true, 4>(X, ld, m, n, tol, tiny2, thr, S);
+        else if (m <= 256) nsweeps = jacobi_groups<32, true, 8>(X, ld, m, n, tol, tiny2, thr, S);
+        else nsweeps = jacobi_groups<32, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
+      } else if (np0 <= 32 || m > 128) {
+        if (m <= 128) nsweeps = jacobi_groups<16, true, 8>(X, ld, m, n, tol, tiny2, thr, S);
+        else nsweeps = jacobi_groups<16, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
+      } else {
+        if (m <= 64) nsweeps = jacobi_groups<8, true, 8>(X, ld, m, n, tol, tiny2, thr, S);
+        else if (m <= 128) nsweeps = jacobi_groups<8, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
+        else nsweeps = jacobi_groups<16, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
+      }
     } else {
-      if (m <= 128) nsweeps = jacobi_groups<8, false>(X, ld, m, n, tol, tiny2, thr, S);
-      else if (m <= 256) nsweeps = jacobi_groups<16, false>(X, ld, m, n, tol, tiny2, thr, S);
-      else nsweeps = jacobi_groups<32, false>(X, ld, m, n, tol, tiny2, thr, S);
+      if (m <= 128) nsweeps = jacobi_groups<8, false, 16>(X, ld, m, n, tol, tiny2, thr, S);
+      else if (m <= 256) nsweeps = jacobi_groups<16, false, 16>(X, ld, m, n, tol, tiny2, thr, S);
+      else nsweeps = jacobi_groups<32, false, 16>(X, ld, m, n, tol, tiny2, thr, S);
     }
   }
   for (int sweep = 0; sweep < MAX_SWEEPS && N > 0 && !(m <= 512); ++sweep) {
@@ -334,5 +423,12 @@ __global__ void __launch_bounds__(NT, 1) svd_kernel(const hq_svd_prob* __restric
 #endif
   }
   (void)nsweeps;
+}
+
+__global__ void __launch_bounds__(NT, 1) svd_kernel(const hq_svd_prob* __restrict__ probs,
+                                                    int* __restrict__ rank,
+                                                    const double* __restrict__ scal) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  svd_single(probs[blockIdx.x], rank, scal, *reinterpret_cast<SvdSmem*>(smem_raw));
 }
 }  // namespace

@@ -772,6 +772,7 @@ class Builder:
 
 SVD_SMEM_DOUBLES = 24576   # single-CTA staging capacity (hq_svd_kernel.cuh)
 CLUSTER_BUF_DOUBLES = 22528  # per-CTA block buffers (hq_svd_cluster.cuh)
+SVD_SINGLE_MAX_PAIRS = 16     # HQ_SVD_SINGLE_MAX_PAIRS (hq_svd_cluster.cuh)
 
 
 def qr_cluster(qr_probs):
@@ -787,20 +788,18 @@ def qr_cluster(qr_probs):
 
 
 def svd_cluster(svd_probs):
-    """Pick single-CTA or cluster Jacobi for a launch from the capacities;
-    launches with many problems already fill the GPU one CTA each."""
+    """Cluster size for a Jacobi launch.  Launches with many problems already
+    fill the GPU one CTA each; few-problem launches get an 8-CTA cluster and
+    the kernel picks one SM, the cluster, or the global-memory path from the
+    run-time core size (capacities overstate it)."""
     mmax = max(p[5].cap for p in svd_probs)
-    if len(svd_probs) > 18:
-        return dict(cluster=1, max_m=mmax)
     nmax = max(min(p[5].cap, p[6].cap) for p in svd_probs)
     ld = (mmax + 1) // 2 * 2
-    if ld * nmax <= SVD_SMEM_DOUBLES or mmax > 512:
+    if len(svd_probs) > 18 or mmax > 512:
         return dict(cluster=1, max_m=mmax)
-    for g in (2, 4, 8):
-        bs = -(-nmax // (2 * g))
-        if 4 * bs * ld <= CLUSTER_BUF_DOUBLES and bs <= 64:
-            return dict(cluster=g, max_m=mmax)
-    return dict(cluster=1, max_m=mmax)
+    if ld * nmax <= SVD_SMEM_DOUBLES and (nmax + 1) // 2 <= SVD_SINGLE_MAX_PAIRS:
+        return dict(cluster=1, max_m=mmax)
+    return dict(cluster=8, max_m=mmax)
 
 
 def _addr(buf, bases, base_ptr):

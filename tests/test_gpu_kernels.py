@@ -108,11 +108,9 @@ def test_qr_and_applyq(dev, m, k, cl):
 def test_svd_truncation(dev, m, n, keep, xform, CL):
     if xform == 0 and m >= 150:
         pytest.skip("unpreconditioned Jacobi is not used by the plan at this size")
+    # cluster launches pick one SM / the cluster / the global-memory path from
+    # the run-time size, so every (size, cluster) combination must be exact
     MM = m
-    if CL > 1:
-        ld, bs = (m + 1) // 2 * 2, -(-min(m, n) // (2 * CL))
-        if 4 * bs * ld > 22528 or bs > 64 or m > 512:
-            pytest.skip("cluster too small for this size (the plan never picks it)")
     torch, lib = dev
     rng = np.random.default_rng(m * n)
     u = np.linalg.qr(rng.standard_normal((m, min(m, n))))[0]
