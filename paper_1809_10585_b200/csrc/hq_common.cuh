@@ -53,3 +53,33 @@ HQ_DEV void dmma884(double& d0, double& d1, double a, double b) {
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
+
+// 8-byte asynchronous global -> shared copy (all in flight; completed by
+// cp_async_wait_all + a barrier)
+HQ_DEV void cp_async8(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+HQ_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// d += A(8 x K) B(K x 8) over k in [kb, ke) on the FP64 tensor pipe with a
+// two-stage register pipeline: the operands of the next 32 k-steps are in
+// flight while the current 8 mma.sync run.  fetch(k0, av, bv) fills the
+// operands of k-steps k0 .. k0+31 (lane's k = k0 + 4u + (lane & 3)).
+template <class F>
+HQ_DEV void dmma_kloop(double& d0, double& d1, int kb, int ke, F fetch) {
+  if (kb >= ke) return;
+  double av[8], bv[8];
+  fetch(kb, av, bv);
+  for (int k0 = kb; k0 < ke; k0 += 32) {
+    double an[8], bn[8];
+    const bool more = k0 + 32 < ke;
+    if (more) fetch(k0 + 32, an, bn);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
+    if (more) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { av[u] = an[u]; bv[u] = bn[u]; }
+    }
+  }
+}

@@ -12,6 +12,13 @@ namespace cg = cooperative_groups;
 
 #ifdef HQ_DEBUG_TIMING
 __device__ long long* hq_dbg = nullptr;
+#define HQ_T0 long long hq_t_ = clock64();
+#define HQ_TMARK(k) do { if (threadIdx.x == 0 && hq_dbg) { const long long c_ = clock64(); atomicAdd((unsigned long long*)(hq_dbg + 2048 + (k)), (unsigned long long)(c_ - hq_t_)); atomicAdd((unsigned long long*)(hq_dbg + 2064 + (k)), 1ull); hq_t_ = c_; } } while (0)
+#else
+#define HQ_T0
+#define HQ_TMARK(k) do { } while (0)
+#endif
+#ifdef HQ_DEBUG_TIMING
 extern "C" int hq_debug_set(void* p) {
   return (int)cudaMemcpyToSymbol(hq_dbg, &p, sizeof(p));
 }
@@ -19,92 +26,38 @@ extern "C" int hq_debug_set(void* p) {
 namespace {
 constexpr int NT = 256, NW = NT / 32, NB = 16;
 constexpr int STAGE_ROWS = 1024;  // panel staged in smem when rows <= STAGE_ROWS
-constexpr int CW = 64;            // trailing-update column chunk
+constexpr int CW = 32;            // trailing-update column chunk
 constexpr int MAXK_T = 384;       // max columns when the full compact-WY T is formed
-constexpr int KPARTS = 4;         // row splits of W = Y^T X when tiles < warps
+constexpr int YBUF = 528 * NB;    // staged Y / X chunk / merge scratch (doubles)
+constexpr int XS_LD = 388;        // merge scratch leading dim (== 4 mod 16)
+// W = Y^T X is kept transposed (wc[col + refl * WLD]) and T^op W as
+// wc2[refl + col * W2LD]: both padded so the m8n8k4 fragment fetches and the
+// per-thread triangular products are bank-conflict free
+constexpr int WLD = CW + 4, W2LD = NB + 4;
+constexpr int WC_OFF = 0, WC2_OFF = NB * WLD, WPART_OFF = WC2_OFF + CW * W2LD;
+constexpr int WSP = WPART_OFF + (NW - 1) * NB * 8;   // k-split partial tiles (16 x 8 each)
+
+// shared-memory leading dimension for staged columns: >= rows and == 4 (mod
+// 16 doubles), so the 8-column x 4-row operand fetches of the m8n8k4 tiles
+// hit 32 distinct banks (a multiple of 16 puts all 8 columns in one bank)
+__host__ __device__ __forceinline__ int pad_ld(int rows) { return ((rows + 11) & ~15) + 4; }
 
 struct QrSmem {
-  double panel[STAGE_ROWS * NB];
+  double panel[(STAGE_ROWS + 4) * NB];  // staged panel being factored / staged X block
+  double ybuf[YBUF];              // staged Y of the previous panel (cluster), X chunks
+                                  // (single-CTA trailing update), X of the T merge
+  double bcast[STAGE_ROWS];       // y_j broadcast of the register-cached panel factorization
   double tp[NB * NB];
   double dmat[NB * NB];   // dmat[c*NB + j] = y_c^T y_j (panel T recurrence)
   double dv[NB];
   double tcol[NB];
-  double wc[NB * CW];
-  double wc2[NB * CW];
-  double wpart[(KPARTS - 1) * NB * CW];
-  double xs[MAXK_T * NB];   // X = Y[:,0:p0]^T Y_p, then X T_p (full-T merge)
+  double wsp[WSP];      // W = Y^T X (wc), T^op W (wc2), k-split partials; 2nd y_j broadcast buffer
   double red[32];
   double scal[4];
 };
 
-// Factor panel P (rows x pw, leading dim ldp; smem or global) into R + unit
-// lower reflectors, gammas into tau[0..pw), and its T factor into S.tp.
-// Column c of the panel is owned by warp c % NW: the owner forms reflector j
-// with warp-level reductions, one CTA barrier publishes it, then every warp
-// applies it to its own columns (dots with warp shuffles) and records the
-// y_c^T y_j products of the T recurrence (wy.py:37-39) -- one barrier per
-// column instead of a block-wide reduction per step.
-__device__ void panel_factor(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  for (int j = 0; j < pw; ++j) {
-    if (wid == (j % NW)) {
-      double* cj = P + (size_t)j * ldp;
-      double ss = 0.0;
-      for (int i = j + 1 + lane; i < rows; i += 32) ss = fma(cj[i], cj[i], ss);
-      ss = warp_sum(ss);
-      const double x0 = cj[j];
-      const double nrm = sqrt(x0 * x0 + ss);
-      double gamma = 0.0, rho = 0.0, inv = 0.0;
-      if (nrm != 0.0) {
-        const double sg = x0 < 0.0 ? -1.0 : 1.0;   // sign(0) := +1
-        const double u1 = x0 + sg * nrm;           // no cancellation
-        rho = -sg * nrm;
-        inv = 1.0 / u1;
-        gamma = 2.0 / (1.0 + ss * inv * inv);
-      }
-      for (int i = j + 1 + lane; i < rows; i += 32) cj[i] *= inv;
-      __syncwarp();
-      if (lane == 0) {
-        cj[j] = rho;
-        S.dv[j] = gamma;
-        tau[j] = gamma;
-      }
-    }
-    __syncthreads();
-    const double gamma = S.dv[j];
-    const double* yj = P + (size_t)j * ldp;
-    for (int c = wid; c < pw; c += NW) {
-      if (c == j) continue;
-      double* cc = P + (size_t)c * ldp;
-      double d = 0.0;
-      for (int i = j + lane; i < rows; i += 32) d = fma(i == j ? 1.0 : yj[i], cc[i], d);
-      d = warp_sum(d);
-      if (c > j) {
-        const double gd = gamma * d;
-        for (int i = j + lane; i < rows; i += 32) cc[i] -= gd * (i == j ? 1.0 : yj[i]);
-      } else if (lane == 0) {
-        S.dmat[c * NB + j] = d;   // y_c^T y_j  (c < j)
-      }
-    }
-  }
-  __syncthreads();
-  // T (pw x pw): T[j][j] = gamma_j, T[0:j, j] = -gamma_j T[0:j,0:j] d[0:j, j]
-  if (wid == 0) {
-    for (int j = 0; j < pw; ++j) {
-      double v = 0.0;
-      if (lane < j) {
-        for (int a = lane; a < j; ++a) v = fma(S.tp[lane + a * NB], S.dmat[a * NB + j], v);
-      }
-      __syncwarp();
-      if (lane < j) S.tp[lane + j * NB] = -S.dv[j] * v;
-      if (lane == j) S.tp[j + j * NB] = S.dv[j];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-}
-
 // column j's reflector, formed by the warp that caches column j in `c`
+// (the diagonal entry x0 comes from its owning lane with one shuffle)
 template <int E>
 __device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int lane, double* ybuf,
                                            double* tau, QrSmem& S) {
@@ -114,10 +67,10 @@ __device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int 
     const int i = lane + 32 * e;
     const double v = c[e];
     if (i > j && i < rows) ss = fma(v, v, ss);
-    if (i == j) x0 = v;
+    if (e == (j >> 5)) x0 = v;
   }
+  x0 = __shfl_sync(0xffffffffu, x0, j & 31);
   ss = warp_sum(ss);
-  x0 = warp_sum(x0);
   const double nrm = sqrt(x0 * x0 + ss);
   double gamma = 0.0, rho = 0.0, inv = 0.0;
   if (nrm != 0.0) {
@@ -139,10 +92,13 @@ __device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int 
 
 // Register-cached variant: warp w holds columns w and w+NW of the panel in
 // registers (lane l owns rows l, l+32, ...; E rows per lane), so a column
-// step is register arithmetic plus one shared-memory broadcast of y_j.
+// step is register arithmetic plus one shared-memory broadcast of y_j.  The
+// broadcast buffer alternates between two arrays, so one barrier per column
+// suffices (the next owner writes the other buffer while y_j is still read).
 template <int E>
-__device__ void panel_factor_reg(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
+__device__ __noinline__ void panel_factor_reg(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  HQ_T0
   double col[2][E];
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
@@ -153,8 +109,8 @@ __device__ void panel_factor_reg(double* P, int ldp, int rows, int pw, double* t
       col[q][e] = (c < pw && i < rows) ? P[i + (size_t)c * ldp] : 0.0;
     }
   }
-  double* ybuf = S.xs;  // broadcast buffer for y_j (rows <= 32 E)
   for (int j = 0; j < pw; ++j) {
+    double* ybuf = (j & 1) ? S.wsp : S.bcast;  // y_j broadcast (rows <= 32 E)
     if (wid == (j % NW)) {
       if (j < NW) own_column<E>(col[0], j, rows, lane, ybuf, tau, S);
       else own_column<E>(col[1], j, rows, lane, ybuf, tau, S);
@@ -164,27 +120,38 @@ __device__ void panel_factor_reg(double* P, int ldp, int rows, int pw, double* t
     double y[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) y[e] = ybuf[lane + 32 * e];
+    // both cached columns: dots first, then the two reductions interleaved
+    double d[2];
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
-      const int c = wid + q * NW;
-      if (c >= pw || c == j) continue;
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
       for (int e = 0; e < E; e += 2) {
         d0 = fma(y[e], col[q][e], d0);
         if (e + 1 < E) d1 = fma(y[e + 1], col[q][e + 1], d1);
       }
-      const double d = warp_sum(d0 + d1);
+      d[q] = d0 + d1;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      d[0] += __shfl_xor_sync(0xffffffffu, d[0], o);
+      d[1] += __shfl_xor_sync(0xffffffffu, d[1], o);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int c = wid + q * NW;
+      if (c >= pw || c == j) continue;
       if (c > j) {
-        const double gd = gamma * d;
+        const double gd = gamma * d[q];
 #pragma unroll
         for (int e = 0; e < E; ++e) col[q][e] = fma(-gd, y[e], col[q][e]);
       } else if (lane == 0) {
-        S.dmat[c * NB + j] = d;   // y_c^T y_j  (c < j)
+        S.dmat[c * NB + j] = d[q];   // y_c^T y_j  (c < j)
       }
     }
-    __syncthreads();   // ybuf reused by the next column
   }
+  __syncthreads();
+  HQ_TMARK(8);
 #pragma unroll
   for (int q = 0; q < 2; ++q) {
     const int c = wid + q * NW;
@@ -195,19 +162,27 @@ __device__ void panel_factor_reg(double* P, int ldp, int rows, int pw, double* t
     }
   }
   // T (pw x pw): T[j][j] = gamma_j, T[0:j, j] = -gamma_j T[0:j,0:j] d[0:j, j]
+  // (wy.py:37-39); lane i keeps row i of T in registers
   if (wid == 0) {
-    for (int j = 0; j < pw; ++j) {
-      double v = 0.0;
-      if (lane < j) {
-        for (int a2 = lane; a2 < j; ++a2) v = fma(S.tp[lane + a2 * NB], S.dmat[a2 * NB + j], v);
+    double trow[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < j; ++l) {
+        const double dl = S.dmat[l * NB + j];
+        if (l & 1) v1 = fma(trow[l], dl, v1); else v0 = fma(trow[l], dl, v0);
       }
-      __syncwarp();
-      if (lane < j) S.tp[lane + j * NB] = -S.dv[j] * v;
-      if (lane == j) S.tp[j + j * NB] = S.dv[j];
-      __syncwarp();
+      const double gj = j < pw ? S.dv[j] : 0.0;
+      trow[j] = j < pw ? (lane < j ? -gj * (v0 + v1) : (lane == j ? gj : 0.0)) : 0.0;
+    }
+    if (lane < NB) {
+#pragma unroll
+      for (int j = 0; j < NB; ++j) S.tp[lane + j * NB] = trow[j];
     }
   }
   __syncthreads();
+  HQ_TMARK(9);
 }
 
 // Block-wide variant for tall panels left in global memory: every warp
@@ -286,108 +261,162 @@ __device__ __forceinline__ double yval(const double* P, int ldp, int i, int a) {
   return i > a ? v : (i == a ? 1.0 : 0.0);
 }
 
+// stage cols columns of rows rows (global, ld lds) into shared dst (ld ldd)
+// with asynchronous copies; ends with a barrier
+__device__ __forceinline__ void stage_cols(double* dst, int ldd, const double* src, int lds, int rows, int cols) {
+  for (int c = 0; c < cols; ++c)
+    for (int i = threadIdx.x; i < rows; i += NT) cp_async8(dst + i + (size_t)c * ldd, src + i + (size_t)c * lds);
+  cp_async_wait_all();
+  __syncthreads();
+}
+
 // X (rows x ncols) := (I - Y T^op Y^T) X for panel reflectors Y (rows x pw,
 // unit diagonal at local row a; smem or global) with T factor tp (NB x NB).
 // trans_t: T^T (applies Q^T) else T (applies Q).  Both products run on the
-// FP64 tensor pipe (mma.sync m8n8k4): W = Y^T X (16 x CW), W2 = T^op W,
-// X -= Y W2, column chunks of CW.
+// FP64 tensor pipe (mma.sync m8n8k4): W = Y^T X (16 x cw), W2 = T^op W,
+// X -= Y W2, column chunks of cw.  When X is in global memory and a staging
+// buffer xs (xs_cap doubles) is given, each chunk is first staged into shared
+// memory with asynchronous copies (one round trip to L2 instead of one per
+// k-block); the result goes back to X.
 template <class SM>
-__device__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, const double* tp,
-                                 double* X, int ldx, int ncols, bool trans_t, SM& S) {
+__device__ __noinline__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, const double* tp,
+                                              double* X, int ldx, int ncols, bool trans_t, SM& S,
+                                              double* xs = nullptr, int xs_cap = 0) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int gq = lane >> 2, tq = lane & 3;
-  for (int c0 = 0; c0 < ncols; c0 += CW) {
-    const int cw = min(CW, ncols - c0);
-    // ---- W = Y^T X_chunk : 2 x ntn output tiles of 8x8; when there are fewer
-    // tiles than warps the row range is split and the partials summed
-    const int ntn = (cw + 7) / 8, tiles = 2 * ntn;
-    const int kparts = max(1, min(KPARTS, NW / tiles));
+  int cwmax = CW;
+  const int ldxs = pad_ld(rows);
+  if (xs) {
+    cwmax = min(CW, (xs_cap / ldxs) & ~7);
+    if (cwmax < 8) { xs = nullptr; cwmax = CW; }
+  }
+  HQ_T0
+  for (int c0 = 0; c0 < ncols; c0 += cwmax) {
+    const int cw = min(cwmax, ncols - c0);
+    const double* Xr = X + (size_t)c0 * ldx;
+    int ldr = ldx;
+    if (xs) {
+      stage_cols(xs, ldxs, Xr, ldx, rows, cw);
+      Xr = xs;
+      ldr = ldxs;
+    }
+    // ---- W = Y^T X_chunk (16 x cw): item (nt, kp) = both 8-reflector halves
+    // against column tile nt over row range kp (the rows are split so that
+    // every warp has an item); two accumulator sets halve the mma chain
+    const int ntn = (cw + 7) / 8;
+    const int kparts = max(1, NW / ntn);
     const int kchunk = ((rows + kparts - 1) / kparts + 31) & ~31;
-    for (int item = wid; item < tiles * kparts; item += NW) {
-      const int tile = item % tiles, kp = item / tiles;
-      const int mt = tile & 1, nt = tile >> 1;
-      double d0 = 0.0, d1 = 0.0;
-      const int a = mt * 8 + gq;          // A row  (reflector index)
+    double* wc = S.wsp + WC_OFF;
+    double* wc2 = S.wsp + WC2_OFF;
+    double* wpart = S.wsp + WPART_OFF;
+    for (int item = wid; item < ntn * kparts; item += NW) {
+      const int nt = item % ntn, kp = item / ntn;
+      double d00 = 0.0, d01 = 0.0, d10 = 0.0, d11 = 0.0;
+      double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0;
       const int j = nt * 8 + gq;          // B col  (chunk column)
-      const double* xc = X + (size_t)(c0 + j) * ldx;
+      const double* xc = Xr + (size_t)(j < cw ? j : 0) * ldr;
       const int kb = kp * kchunk, ke = min(rows, kb + kchunk);
-      // loads for 8 k-steps issued back to back, then 8 DMMAs (latency hiding)
       for (int k0 = kb; k0 < ke; k0 += 32) {
-        double av[8], bv[8];
+        double a0[8], a1[8], bv[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int ia = k0 + 4 * u + tq;
-          av[u] = (ia < ke && a < pw) ? yval(Y, ldy, ia, a) : 0.0;
-          bv[u] = (ia < ke && j < cw) ? xc[ia] : 0.0;
+          const bool in = ia < ke;
+          a0[u] = (in && gq < pw) ? yval(Y, ldy, ia, gq) : 0.0;
+          a1[u] = (in && 8 + gq < pw) ? yval(Y, ldy, ia, 8 + gq) : 0.0;
+          bv[u] = (in && j < cw) ? xc[ia] : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
+        for (int u = 0; u < 8; u += 2) {
+          dmma884(d00, d01, a0[u], bv[u]);
+          dmma884(d10, d11, a1[u], bv[u]);
+          dmma884(e00, e01, a0[u + 1], bv[u + 1]);
+          dmma884(e10, e11, a1[u + 1], bv[u + 1]);
+        }
       }
-      const int r = mt * 8 + gq, cc = nt * 8 + 2 * tq;
-      double* wp = kp == 0 ? S.wc : S.wpart + (kp - 1) * NB * CW;
-      wp[r + cc * NB] = d0;
-      wp[r + (cc + 1) * NB] = d1;
+      const int cl = 2 * tq;   // column within the tile
+      if (kp == 0) {
+        const int cc = nt * 8 + cl;
+        wc[cc + gq * WLD] = d00 + e00;
+        wc[cc + 1 + gq * WLD] = d01 + e01;
+        wc[cc + (8 + gq) * WLD] = d10 + e10;
+        wc[cc + 1 + (8 + gq) * WLD] = d11 + e11;
+      } else {
+        double* wp = wpart + ((kp - 1) * ntn + nt) * NB * 8;
+        wp[cl + gq * 8] = d00 + e00;
+        wp[cl + 1 + gq * 8] = d01 + e01;
+        wp[cl + (8 + gq) * 8] = d10 + e10;
+        wp[cl + 1 + (8 + gq) * 8] = d11 + e11;
+      }
     }
     __syncthreads();
-    if (kparts > 1)
-      for (int e = t; e < NB * cw; e += NT)
-        for (int kp = 1; kp < kparts; ++kp) S.wc[e] += S.wpart[(kp - 1) * NB * CW + e];
-    if (kparts > 1) __syncthreads();
+    HQ_TMARK(0);
+    if (kparts > 1) {
+      for (int e = t; e < NB * cw; e += NT) {
+        const int a = e / cw, cc = e % cw, nt = cc >> 3;
+        double v = wc[cc + a * WLD];
+        for (int kp = 1; kp < kparts; ++kp) v += wpart[((kp - 1) * ntn + nt) * NB * 8 + (cc & 7) + a * 8];
+        wc[cc + a * WLD] = v;
+      }
+      __syncthreads();
+    }
+    // W2 = T^op W: thread (a, cc); lanes run along cc (T entries broadcast)
     for (int e = t; e < NB * cw; e += NT) {
-      const int a = e % NB, cc = e / NB;
+      const int a = e / cw, cc = e % cw;
       double v = 0.0;
       if (a < pw) {
-        if (trans_t) { for (int b = 0; b <= a; ++b) v = fma(tp[b + a * NB], S.wc[b + cc * NB], v); }
-        else { for (int b = a; b < pw; ++b) v = fma(tp[a + b * NB], S.wc[b + cc * NB], v); }
+        if (trans_t) { for (int b = 0; b <= a; ++b) v = fma(tp[b + a * NB], wc[cc + b * WLD], v); }
+        else { for (int b = a; b < pw; ++b) v = fma(tp[a + b * NB], wc[cc + b * WLD], v); }
       }
-      S.wc2[a + cc * NB] = v;
+      wc2[a + cc * W2LD] = v;
     }
     __syncthreads();
-    // ---- X_chunk -= Y W2 : (rows/8) x (cw/8) tiles, k = NB; four tiles per
-    // warp iteration with all their loads issued before the DMMAs
-    const int ntm = (rows + 7) / 8, ntt = ntm * ntn;
-    for (int base = wid; base < ntt; base += 4 * NW) {
-      double d0[4], d1[4], av[4][4], bv[4][4];
+    HQ_TMARK(1);
+    // ---- X_chunk -= Y W2 : warp w takes row tiles mt = w, w + NW, ...; the
+    // W2 fragments of all column tiles stay in registers, the Y fragment of a
+    // row tile is loaded once for all its column tiles
+    double* Xw = X + (size_t)c0 * ldx;
+    const int ntm = (rows + 7) / 8;
+    double bw[CW / 8][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int tile = base + u * NW;
-        const bool ok = tile < ntt;
-        const int mt = ok ? tile % ntm : 0, nt = ok ? tile / ntm : 0;
-        const int i = mt * 8 + gq, j = nt * 8 + 2 * tq;
-        const double* x0 = X + (size_t)(c0 + j) * ldx;
-        d0[u] = (ok && i < rows && j < cw) ? x0[i] : 0.0;
-        d1[u] = (ok && i < rows && j + 1 < cw) ? x0[ldx + i] : 0.0;
-        const int ib = mt * 8 + gq, jb = nt * 8 + gq;
+    for (int nt = 0; nt < CW / 8; ++nt)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int a = 4 * q + tq;
-          av[u][q] = (ok && ib < rows && a < pw) ? -yval(Y, ldy, ib, a) : 0.0;
-          bv[u][q] = (ok && jb < cw) ? S.wc2[a + jb * NB] : 0.0;
-        }
+      for (int q = 0; q < 4; ++q) {
+        const int jb = nt * 8 + gq;
+        bw[nt][q] = (nt < ntn && jb < cw) ? wc2[4 * q + tq + jb * W2LD] : 0.0;
+      }
+#pragma unroll 2
+    for (int mt = wid; mt < ntm; mt += NW) {
+      const int i = mt * 8 + gq;
+      double av[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int a = 4 * q + tq;
+        av[q] = (i < rows && a < pw) ? -yval(Y, ldy, i, a) : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int nt = 0; nt < CW / 8; ++nt) {
+        if (nt >= ntn) break;
+        const int j = nt * 8 + 2 * tq;
+        const double* x0 = Xr + (size_t)j * ldr;
+        double d0 = (i < rows && j < cw) ? x0[i] : 0.0;
+        double d1 = (i < rows && j + 1 < cw) ? x0[ldr + i] : 0.0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dmma884(d0[u], d1[u], av[u][q], bv[u][q]);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int tile = base + u * NW;
-        if (tile >= ntt) continue;
-        const int mt = tile % ntm, nt = tile / ntm;
-        const int i = mt * 8 + gq, j = nt * 8 + 2 * tq;
-        double* x0 = X + (size_t)(c0 + j) * ldx;
-        if (i < rows && j < cw) x0[i] = d0[u];
-        if (i < rows && j + 1 < cw) x0[ldx + i] = d1[u];
+        for (int q = 0; q < 4; ++q) dmma884(d0, d1, av[q], bw[nt][q]);
+        double* xo = Xw + (size_t)j * ldx;
+        if (i < rows && j < cw) xo[i] = d0;
+        if (i < rows && j + 1 < cw) xo[ldx + i] = d1;
       }
     }
     __syncthreads();
+    HQ_TMARK(2);
   }
 }
 
 // Merge panel p0 (reflectors P, ld ldp; T factor tp) into the full
 // compact-WY T: T[0:p0, p] = -T[0:p0,0:p0] (Y[:,0:p0]^T Y_p) T_p (wy.py:53).
 // Needs the T blocks of all earlier panels.
-__device__ void merge_T(const hq_qr_prob& Q, const double* W, int ld, int m, int r, int p0,
+__device__ __noinline__ void merge_T(const hq_qr_prob& Q, const double* W, int ld, int m, int r, int p0,
                         const double* P, int ldp, const double* tpv, QrSmem& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int pw = min(NB, r - p0), rows = m - p0;
@@ -405,33 +434,30 @@ __device__ void merge_T(const hq_qr_prob& Q, const double* W, int ld, int m, int
           const int mt = tile >> 1, nt = tile & 1;
           const int b = mt * 8 + gq, a = nt * 8 + gq;
           double d0 = 0.0, d1 = 0.0;
-          for (int k0 = 0; k0 < rows; k0 += 32) {
-            double av[8], bv[8];
+          dmma_kloop(d0, d1, 0, rows, [&](int k0, double (&av)[8], double (&bv)[8]) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int i = k0 + 4 * u + tq;
               av[u] = (i < rows && b < p0) ? W[(p0 + i) + (size_t)b * ld] : 0.0;
               bv[u] = (i < rows && a < pw) ? yval(P, ldp, i, a) : 0.0;
             }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
-          }
+          });
           const int r = mt * 8 + gq, c = nt * 8 + 2 * tq;
-          if (r < p0) { S.xs[r + c * MAXK_T] = d0; S.xs[r + (c + 1) * MAXK_T] = d1; }
+          if (r < p0) { S.ybuf[r + c * XS_LD] = d0; S.ybuf[r + (c + 1) * XS_LD] = d1; }
         }
         __syncthreads();
         // X := X T_p (in place per row)
         for (int b = t; b < p0; b += NT) {
           double xr[NB];
 #pragma unroll
-          for (int a = 0; a < NB; ++a) xr[a] = a < pw ? S.xs[b + a * MAXK_T] : 0.0;
+          for (int a = 0; a < NB; ++a) xr[a] = a < pw ? S.ybuf[b + a * XS_LD] : 0.0;
 #pragma unroll
           for (int a = 0; a < NB; ++a) {
             double v = 0.0;
 #pragma unroll
             for (int c = 0; c < NB; ++c)
               if (c <= a) v = fma(xr[c], tp_[c + a * NB], v);
-            if (a < pw) S.xs[b + a * MAXK_T] = v;
+            if (a < pw) S.ybuf[b + a * XS_LD] = v;
           }
         }
         __syncthreads();
@@ -440,17 +466,14 @@ __device__ void merge_T(const hq_qr_prob& Q, const double* W, int ld, int m, int
           const int mt = tile >> 1, nt = tile & 1;
           const int r = mt * 8 + gq, a = nt * 8 + gq;
           double d0 = 0.0, d1 = 0.0;
-          for (int k0 = mt * 8; k0 < p0; k0 += 32) {
-            double av[8], bv[8];
+          dmma_kloop(d0, d1, mt * 8, p0, [&](int k0, double (&av)[8], double (&bv)[8]) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
               const int c = k0 + 4 * u + tq;
               av[u] = (r < p0 && c < p0 && c >= r) ? -TF[r + (size_t)c * ldt] : 0.0;
-              bv[u] = (c < p0 && a < pw) ? S.xs[c + a * MAXK_T] : 0.0;
+              bv[u] = (c < p0 && a < pw) ? S.ybuf[c + a * XS_LD] : 0.0;
             }
-#pragma unroll
-            for (int u = 0; u < 8; ++u) dmma884(d0, d1, av[u], bv[u]);
-          }
+          });
           const int ro = mt * 8 + gq, co = nt * 8 + 2 * tq;
           if (ro < p0 && co < pw) TF[ro + (size_t)(p0 + co) * ldt] = d0;
           if (ro < p0 && co + 1 < pw) TF[ro + (size_t)(p0 + co + 1) * ldt] = d1;
@@ -461,42 +484,51 @@ __device__ void merge_T(const hq_qr_prob& Q, const double* W, int ld, int m, int
   }
 }
 
+// Reduce panel p0 held at P (rows x pw, ld ldp; shared or global) into R +
+// unit lower reflectors; publish gamma (tau) and T_p (S.tp, Q.tpanel).
+__device__ void factor_panel_core(const hq_qr_prob& Q, double* P, int ldp, int rows, int pw, int p0,
+                                  QrSmem& S) {
+  const int t = threadIdx.x;
+  if (t < NB * NB) S.tp[t] = 0.0;
+  __syncthreads();
+  HQ_T0
+  if (rows <= 128) panel_factor_reg<4>(P, ldp, rows, pw, Q.tau + p0, S);
+  else if (rows <= 256) panel_factor_reg<8>(P, ldp, rows, pw, Q.tau + p0, S);
+  else if (rows <= 512) panel_factor_reg<16>(P, ldp, rows, pw, Q.tau + p0, S);
+  else if (rows <= 1024) panel_factor_reg<32>(P, ldp, rows, pw, Q.tau + p0, S);
+  else panel_factor_block(P, ldp, rows, pw, Q.tau + p0, S);
+  HQ_TMARK(5);
+  if (Q.tpanel && t < NB * NB) Q.tpanel[(size_t)(p0 / NB) * NB * NB + t] = S.tp[t];
+}
+
 // Factor panel p0 of problem Q: stage it (when it fits), reduce it, publish
 // gamma / T_p, (single-CTA path: update the trailing columns while the
-// panel is staged), merge T_p into the full compact-WY T when requested,
-// write the panel back.
+// panel is staged, staging chunks of them through S.ybuf), merge T_p into the
+// full compact-WY T when requested, write the panel back.
 __device__ void factor_panel_step(const hq_qr_prob& Q, double* W, int ld, int m, int k, int r, int p0,
                                   bool do_trailing, bool do_merge, QrSmem& S) {
-  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-  {
-    const int pw = min(NB, r - p0), rows = m - p0;
-    double* Pg = W + p0 + (size_t)p0 * ld;
-    const bool staged = rows <= STAGE_ROWS;
-    double* P = Pg;
-    int ldp = ld;
-    if (staged) {
-      P = S.panel; ldp = rows;
-      for (int e = t; e < rows * pw; e += NT) P[e % rows + (e / rows) * ldp] = Pg[e % rows + (size_t)(e / rows) * ld];
-    }
-    if (t < NB * NB) S.tp[t] = 0.0;
-    __syncthreads();
-    if (rows <= 128) panel_factor_reg<4>(P, ldp, rows, pw, Q.tau + p0, S);
-    else if (rows <= 256) panel_factor_reg<8>(P, ldp, rows, pw, Q.tau + p0, S);
-    else if (rows <= 512) panel_factor_reg<16>(P, ldp, rows, pw, Q.tau + p0, S);
-    else if (rows <= 1024) panel_factor_reg<32>(P, ldp, rows, pw, Q.tau + p0, S);
-    else if (staged) panel_factor(P, ldp, rows, pw, Q.tau + p0, S);
-    else panel_factor_block(P, ldp, rows, pw, Q.tau + p0, S);
-    if (Q.tpanel && t < NB * NB) Q.tpanel[(size_t)(p0 / NB) * NB * NB + t] = S.tp[t];
-    // trailing columns: A_trail := Q_p^T A_trail
-    if (do_trailing && p0 + pw < k)
-      apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S);
-    __syncthreads();
-    if (do_merge) merge_T(Q, W, ld, m, r, p0, P, ldp, S.tp, S);
-    if (staged) {
-      for (int e = t; e < rows * pw; e += NT) Pg[e % rows + (size_t)(e / rows) * ld] = P[e % rows + (e / rows) * ldp];
-    }
-    __syncthreads();
+  const int t = threadIdx.x;
+  const int pw = min(NB, r - p0), rows = m - p0;
+  double* Pg = W + p0 + (size_t)p0 * ld;
+  const bool staged = rows <= STAGE_ROWS;
+  double* P = Pg;
+  int ldp = ld;
+  if (staged) {
+    ldp = pad_ld(rows);
+    stage_cols(S.panel, ldp, Pg, ld, rows, pw);
+    P = S.panel;
   }
+  factor_panel_core(Q, P, ldp, rows, pw, p0, S);
+  // trailing columns: A_trail := Q_p^T A_trail
+  if (do_trailing && p0 + pw < k)
+    apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S,
+                     S.ybuf, YBUF);
+  __syncthreads();
+  if (do_merge) merge_T(Q, W, ld, m, r, p0, P, ldp, S.tp, S);
+  if (staged)
+    for (int c = 0; c < pw; ++c)
+      for (int i = t; i < rows; i += NT) Pg[i + (size_t)c * ld] = P[i + c * ldp];
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(NT) qr_kernel(const hq_qr_prob* __restrict__ probs,
@@ -539,41 +571,72 @@ __global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __r
     if (ph >= 1) {
       const int q0 = (ph - 1) * NB, qw = min(NB, r - q0), rows = m - q0;
       if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
-      __syncthreads();
-      const double* Y = W + q0 + (size_t)q0 * ld;
+      const double* Yg = W + q0 + (size_t)q0 * ld;
+      // block assignment of this phase: CTA ph % G updates and factors block
+      // ph alone (its chain bounds the phase); the later blocks go round-robin
+      // to the other CTAs (all CTAs once there is nothing left to factor)
+      const int fct = ph % G;
+      const bool factoring = ph < np;
+      int b0, bstep;
+      if (!factoring) { b0 = ph + cr; bstep = G; }
+      else if (cr == fct) { b0 = ph; bstep = nbk; }
+      else { b0 = ph + 1 + (cr - fct - 1 + G) % G; bstep = G - 1; }
+      const bool partial = ph == np && qw < NB && k > r && ((ph - 1) % G) == cr;
+      const bool busy = b0 < nbk || partial;
+      // panel ph-1 is read once per owned block: stage it (asynchronous
+      // copies, one L2 round trip) when it fits
+      const double* Y = Yg;
+      int ldy = ld;
+      if (busy && pad_ld(rows) * NB <= YBUF) {
+        ldy = pad_ld(rows);
+        stage_cols(S.ybuf, ldy, Yg, ld, rows, qw);
+        Y = S.ybuf;
+      } else {
+        __syncthreads();
+      }
       // a partial last panel (r not a multiple of NB, k > r): the rest of its
       // own block lies beyond the reflectors and still needs panel ph-1
-      if (ph == np && qw < NB && k > r && ((ph - 1) % G) == cr) {
+      if (partial) {
         const int c1 = min(k, q0 + NB);
-        apply_panel_cols(Y, ld, rows, qw, S.tp, W + q0 + (size_t)r * ld, ld, c1 - r, true, S);
+        apply_panel_cols(Y, ldy, rows, qw, S.tp, W + q0 + (size_t)r * ld, ld, c1 - r, true, S, S.panel,
+                         (STAGE_ROWS + 4) * NB);
       }
-      // my blocks b >= ph, block ph first
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int b = ph; b < nbk; ++b) {
-          if (b % G != cr) continue;
-          const bool first = (b == ph);
-          if ((pass == 0) != first) continue;
-          const int c0 = b * NB, cw = min(NB, k - c0);
-          apply_panel_cols(Y, ld, rows, qw, S.tp, W + q0 + (size_t)c0 * ld, ld, cw, true, S);
-        }
-        if (pass == 0 && ph < np && (ph % G) == cr) {
+      for (int b = b0; b < nbk; b += bstep) {
+        const int c0 = b * NB, cw = min(NB, k - c0);
+        double* Xg = W + q0 + (size_t)c0 * ld;
+        if (b == ph && ph < np && rows <= STAGE_ROWS) {
+          // block ph becomes panel ph: stage it, apply panel ph-1 in shared
+          // memory, factor it in place, write it back once
 #ifdef HQ_DEBUG_TIMING
           tB = clock64();
 #endif
-          factor_panel_step(Q, W, ld, m, k, r, ph * NB, false, false, S);
+          const int lds = pad_ld(rows);
+          stage_cols(S.panel, lds, Xg, ld, rows, cw);
+          apply_panel_cols(Y, ldy, rows, qw, S.tp, S.panel, lds, cw, true, S);
+          factor_panel_core(Q, S.panel + NB, lds, rows - NB, min(NB, r - ph * NB), ph * NB, S);
+          __syncthreads();
+          for (int c = 0; c < cw; ++c)
+            for (int i = t; i < rows; i += NT) Xg[i + (size_t)c * ld] = S.panel[i + c * lds];
+          // factoring overwrote S.tp with T_ph: restore T_(ph-1)
+          if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
+          __syncthreads();
 #ifdef HQ_DEBUG_TIMING
           tC = clock64();
 #endif
-          // factoring overwrote S.tp with T_ph: restore T_(ph-1) for pass 1
-          if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
-          __syncthreads();
+        } else {
+          apply_panel_cols(Y, ldy, rows, qw, S.tp, Xg, ld, cw, true, S, S.panel, (STAGE_ROWS + 4) * NB);
+          if (b == ph && ph < np) {
+            factor_panel_step(Q, W, ld, m, k, r, ph * NB, false, false, S);
+            if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
+            __syncthreads();
+          }
         }
       }
       // the full compact-WY T block of panel ph-1 is merged one phase later
       // by a CTA that is not factoring (off the panel chain)
       if (Q.tfull && cr == (ph + 1) % G) {
         __syncthreads();
-        merge_T(Q, W, ld, m, r, q0, Y, ld, S.tp, S);
+        merge_T(Q, W, ld, m, r, q0, Yg, ld, S.tp, S);
       }
     } else if (np > 0 && cr == 0) {
       factor_panel_step(Q, W, ld, m, k, r, 0, false, false, S);
@@ -593,19 +656,23 @@ __global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __r
   }
 }
 
+// grid (problem, column chunk of APQ_CW): the columns of X are independent,
+// so each CTA applies all reflectors to its own chunk.  For m <= APQ_STAGE
+// the chunk stays in shared memory for the whole sweep over the panels and
+// each panel's reflectors are staged with asynchronous copies.
+constexpr int APQ_CW = 32;
+constexpr int APQ_STAGE = 512;
 struct ApqSmem {
   double tp[NB * NB];
-  double wc[NB * CW];
-  double wc2[NB * CW];
-  double wpart[(KPARTS - 1) * NB * CW];
+  double wsp[WSP];
+  double xbuf[(APQ_STAGE + 16) * APQ_CW];
+  double ybuf[(APQ_STAGE + 16) * NB];
 };
 
-// grid (problem, column chunk of APQ_CW): the columns of X are independent,
-// so each CTA applies all reflectors to its own chunk.
-constexpr int APQ_CW = 32;
 __global__ void __launch_bounds__(NT) applyq_kernel(const hq_applyq_prob* __restrict__ probs,
                                                     int* __restrict__ rank) {
-  __shared__ ApqSmem S;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ApqSmem& S = *reinterpret_cast<ApqSmem*>(smem_raw);
   const hq_applyq_prob A = probs[blockIdx.x];
   const int m = hq_dim(rank, A.m, A.m_ri), k = hq_dim(rank, A.k, A.k_ri);
   const int call = hq_dim(rank, A.c, A.c_ri);
@@ -614,25 +681,38 @@ __global__ void __launch_bounds__(NT) applyq_kernel(const hq_applyq_prob* __rest
   const int cbeg = blockIdx.y * APQ_CW;
   if (m <= 0 || cbeg >= call) return;
   const int c = min(APQ_CW, call - cbeg);
-  double* X = A.x + (size_t)cbeg * A.ldx;
+  double* Xg = A.x + (size_t)cbeg * A.ldx;
+  const bool staged = m <= APQ_STAGE;
+  double* X = staged ? S.xbuf : Xg;
+  const int ldx = staged ? pad_ld(m) : A.ldx;
   if (A.x0) {
     const int r0 = hq_dim(rank, A.r0, A.r0_ri);
     const double* X0 = A.x0 + (size_t)cbeg * A.ldx0;
-    for (size_t e = t; e < (size_t)m * c; e += NT) {
-      const int i = (int)(e % m), j = (int)(e / m);
-      X[i + (size_t)j * A.ldx] = i < r0 ? X0[i + (size_t)j * A.ldx0] : 0.0;
-    }
+    for (int j = 0; j < c; ++j)
+      for (int i = t; i < m; i += NT) X[i + (size_t)j * ldx] = i < r0 ? X0[i + (size_t)j * A.ldx0] : 0.0;
     __syncthreads();
+  } else if (staged) {
+    stage_cols(S.xbuf, ldx, Xg, A.ldx, m, c);
   }
   const int np = (r + NB - 1) / NB;
   for (int s = 0; s < np; ++s) {
     const int p = A.trans ? s : np - 1 - s;
     const int p0 = p * NB, pw = min(NB, r - p0), rows = m - p0;
     if (t < NB * NB) S.tp[t] = A.tpanel[(size_t)p * NB * NB + t];
-    __syncthreads();
-    apply_panel_cols(A.w + p0 + (size_t)p0 * A.ldw, A.ldw, rows, pw, S.tp, X + p0, A.ldx, c,
-                     A.trans != 0, S);
+    const double* Y = A.w + p0 + (size_t)p0 * A.ldw;
+    int ldy = A.ldw;
+    if (staged) {
+      ldy = pad_ld(rows);
+      stage_cols(S.ybuf, ldy, Y, A.ldw, rows, pw);
+      Y = S.ybuf;
+    } else {
+      __syncthreads();
+    }
+    apply_panel_cols(Y, ldy, rows, pw, S.tp, X + p0, ldx, c, A.trans != 0, S);
   }
+  if (staged)
+    for (int j = 0; j < c; ++j)
+      for (int i = t; i < m; i += NT) Xg[i + (size_t)j * A.ldx] = X[i + (size_t)j * ldx];
 }
 
 // dst (rows x K) = [alpha_1 P_1 | alpha_2 P_2 | ...]; K -> rank[ktot_ri]
@@ -829,7 +909,14 @@ extern "C" int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, i
                          int max_cols) {
   if (nprob <= 0) return 0;
   const int nchunk = max_cols > 0 ? (max_cols + APQ_CW - 1) / APQ_CW : 1;
-  applyq_kernel<<<dim3(nprob, nchunk), NT, 0, (cudaStream_t)stream>>>(probs, rank);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(applyq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(ApqSmem));
+    if (e != cudaSuccess) return hq_err(e);
+    attr = true;
+  }
+  applyq_kernel<<<dim3(nprob, nchunk), NT, sizeof(ApqSmem), (cudaStream_t)stream>>>(probs, rank);
   return hq_err(cudaGetLastError());
 }
 

@@ -95,3 +95,23 @@ while i >= 0:
     i = pred[i]
 for k, (tm, c) in sorted(cp.items(), key=lambda x: -x[1][0]):
     print(f"  on path: {k:28s} {c:5d} ops {tm:9.1f} ms")
+# on-path detail for one kind: shape buckets
+detail = sys.argv[5] if len(sys.argv) > 5 else None
+if detail:
+    dd = collections.defaultdict(lambda: [0.0, 0])
+    i = end
+    while i >= 0:
+        kind, probs, ex = ops[i]
+        if kind == detail and probs:
+            if kind == "qr":
+                sh = max((_dv(p[6], rk), _dv(p[7], rk)) for p in probs)
+                key = (len(probs), (sh[0] + 63) // 64 * 64, (sh[1] + 15) // 16 * 16, ex.get("cluster", 1) if isinstance(ex, dict) else ex)
+            elif kind == "gemm":
+                key = (len(probs), ex.get("ksplit"), max(max((_dv(t[8], rk) for t in p[5]), default=0) for p in probs) // 64 * 64)
+            else:
+                key = (len(probs),)
+            dd[key][0] += times[i]; dd[key][1] += 1
+        i = pred[i]
+    print(f"on-path {detail} by (nprob, m64, k16, extra):")
+    for k, (tm, c) in sorted(dd.items(), key=lambda x: -x[1][0])[:30]:
+        print(f"    {str(k):40s} {c:4d} ops {tm:8.2f} ms  avg {1000 * tm / c:7.1f} us")
