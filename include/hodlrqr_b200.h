@@ -175,6 +175,13 @@ int hq_device_check(void);
    pre-zeroed C (beta ignored); skip != NULL && *skip != 0 makes it a no-op */
 int hq_gemm(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
             int* rank, int tiles, int ksplit, const int* skip);
+/* the same product for outputs of at most 4 columns (power-iteration
+   blocks^T X, Gram and leaf products).  mode 0: grid (ksplit, nprob), K split
+   evenly over CTAs, with ksplit > 1 C must be zero on entry (atomic
+   accumulation); mode 1: one thread per output row (max_rows bounds m),
+   ksplit ignored */
+int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
+                   int* rank, int ksplit, int ncmax, int mode, int max_rows, const int* skip);
 int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_piece* pieces,
               int* rank, int max_rows);
 /* cluster >= 2: each problem is factored by a cluster of 2/4/8 CTAs (column

@@ -38,6 +38,7 @@ NB = 16          # QR panel width (hq_qr.cu)
 TALL_ROWS = 1024  # factor stacks taller than this are QR'd by one-level TSQR
 TSQR_CH = 512     # TSQR chunk rows (register-cached panels)
 GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
+SKINNY_MAX_COLS = 4  # hq_gemm_skinny: outputs with at most this many columns
 SVD_MAX_N = 1024
 
 R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT, R_SHARED = range(8)
@@ -289,7 +290,19 @@ class Builder:
         tiles = max(math.ceil(p[2].cap / GEMM_TILE) * math.ceil(p[3].cap / GEMM_TILE) for p in probs)
         if tiles <= 0:
             return
-        self.op("gemm", probs, dict(tiles=tiles, ksplit=ksplit, skip=skip))
+        ncmax = max(p[3].cap for p in probs)
+        mmax = max(p[2].cap for p in probs)
+        kmax = max(max(t[8].cap for t in p[5]) for p in probs)
+        # outputs of <= 4 columns (power iteration): the skinny kernels --
+        # threads along K for long K, one thread per output row otherwise
+        skinny = ncmax <= SKINNY_MAX_COLS
+        mode = 0 if (kmax >= 1024 or mmax <= 64) else 1
+        if skinny and mode == 0 and ksplit > 1:
+            # a K-slice of >= 8 k per thread amortizes the CTA reduction
+            # (only ever lowered: the caller zeroed C for ksplit > 1)
+            ksplit = max(1, min(ksplit, kmax // 2048))
+        self.op("gemm", probs, dict(tiles=tiles, ksplit=ksplit, skip=skip, skinny=skinny, ncmax=ncmax,
+                                    mode=mode, max_rows=mmax))
 
     def zero(self, regions):
         if regions:
@@ -1092,7 +1105,11 @@ class CompiledPlan:
         for kind, o1, o2, cnt, ex in launch:
             if kind == "gemm":
                 skip = rk + 4 * ex["skip"] if ex["skip"] is not None else None
-                rc = lib.hq_gemm(stream_handle, dp + o1, cnt, dp + o2, rk, ex["tiles"], ex["ksplit"], skip)
+                if ex.get("skinny"):
+                    rc = lib.hq_gemm_skinny(stream_handle, dp + o1, cnt, dp + o2, rk, ex["ksplit"], ex["ncmax"],
+                                            ex["mode"], ex["max_rows"], skip)
+                else:
+                    rc = lib.hq_gemm(stream_handle, dp + o1, cnt, dp + o2, rk, ex["tiles"], ex["ksplit"], skip)
             elif kind == "zero":
                 rc = lib.hq_zero(stream_handle, dp + o1, cnt, ex["max_count"])
             elif kind == "concat":

@@ -54,6 +54,49 @@ def test_gemm(dev, m, n, k, ta, tb):
     assert np.allclose(back(dC, m, n), ref, atol=1e-12 * max(1, np.abs(ref).max()))
 
 
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("m,n,k,ta,tb,ks,masks", [(16, 2, 8192, 1, 0, 32, (0, 0)), (2, 2, 5000, 1, 0, 19, (0, 0)),
+                                                  (256, 2, 256, 0, 0, 1, (1, 0)), (37, 3, 300, 1, 1, 1, (2, 0)),
+                                                  (70, 4, 900, 0, 1, 4, (0, 0)), (5, 1, 3, 1, 0, 1, (0, 0)),
+                                                  (600, 2, 40, 1, 0, 1, (0, 2))])
+def test_gemm_skinny(dev, m, n, k, ta, tb, ks, masks, mode):
+    """hq_gemm_skinny: two terms, masks, transposes, beta (ks == 1) or
+    atomic split-K into a zeroed C (ks > 1)."""
+    torch, lib = dev
+    rng = np.random.default_rng(m * 7 + n + k)
+    A = rng.standard_normal((k, m) if ta else (m, k))
+    B = rng.standard_normal((n, k) if tb else (k, n))
+    A2 = rng.standard_normal((m, 5))
+    B2 = rng.standard_normal((5, n))
+    if mode == 1:
+        ks = 1
+    C = rng.standard_normal((m, n)) if ks == 1 else np.zeros((m, n))
+    dA, dB, dA2, dB2, dC = (colmajor(torch, x) for x in (A, B, A2, B2, C))
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    terms = np.zeros(2, _abi.GEMM_TERM)
+    terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, masks[0], masks[1], 0.75)
+    terms[1] = (dA2.data_ptr(), dB2.data_ptr(), m, 5, 0, 0, 5, -1, 0, 0, -1.0)
+    probs = np.zeros(1, _abi.GEMM_PROB)
+    beta = 0.5 if ks == 1 else 0.0
+    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta)
+    dt, dp = put(torch, terms), put(torch, probs)
+    assert lib.hq_gemm_skinny(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), ks, n, mode, m, None) == 0
+    torch.cuda.synchronize()
+
+    def mask(x, mk):
+        if mk == 1:
+            return np.triu(x)
+        if mk == 2:
+            y = np.tril(x, -1)
+            np.fill_diagonal(y, 1.0)
+            return y
+        return x
+    opA = (mask(A, masks[0])).T if ta else mask(A, masks[0])
+    opB = (mask(B, masks[1])).T if tb else mask(B, masks[1])
+    ref = beta * C + 0.75 * (opA @ opB) - A2 @ B2
+    assert np.allclose(back(dC, m, n), ref, atol=1e-11 * max(1, np.abs(ref).max()))
+
+
 @pytest.mark.parametrize("cl", [1, 2, 8])
 @pytest.mark.parametrize("m,k", [(25, 25), (28, 25), (9, 6), (300, 40), (50, 70), (1200, 17), (200, 200), (60, 57),
                                  (352, 256)])

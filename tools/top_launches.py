@@ -107,7 +107,10 @@ if detail:
                 sh = max((_dv(p[6], rk), _dv(p[7], rk)) for p in probs)
                 key = (len(probs), (sh[0] + 63) // 64 * 64, (sh[1] + 15) // 16 * 16, ex.get("cluster", 1) if isinstance(ex, dict) else ex)
             elif kind == "gemm":
-                key = (len(probs), ex.get("ksplit"), max(max((_dv(t[8], rk) for t in p[5]), default=0) for p in probs) // 64 * 64)
+                mm = max(_dv(p[2], rk) for p in probs); nn = max(_dv(p[3], rk) for p in probs)
+                kk = max(max((_dv(t[8], rk) for t in p[5]), default=0) for p in probs)
+                nterm = max(len(p[5]) for p in probs)
+                key = (len(probs), ex.get("ksplit"), "m%d" % ((mm + 63) // 64 * 64), "n%d" % ((nn + 15) // 16 * 16), "k%d" % ((kk + 63) // 64 * 64), "t%d" % nterm)
             else:
                 key = (len(probs),)
             dd[key][0] += times[i]; dd[key][1] += 1
