@@ -175,6 +175,10 @@ int hq_device_check(void);
    pre-zeroed C (beta ignored); skip != NULL && *skip != 0 makes it a no-op */
 int hq_gemm(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
             int* rank, int tiles, int ksplit, const int* skip);
+/* hq_gemm with the output tile size chosen (tile = 32 or 64; tiles counts
+   tile x tile blocks): small products use 32 x 32 tiles to occupy more SMs */
+int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
+                  int* rank, int tiles, int ksplit, int tile, const int* skip);
 /* the same product for outputs of at most 4 columns (power-iteration
    blocks^T X, Gram and leaf products).  mode 0: grid (ksplit, nprob), K split
    evenly over CTAs, with ksplit > 1 C must be zero on entry (atomic

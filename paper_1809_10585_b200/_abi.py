@@ -53,7 +53,7 @@ STRUCT_SIZES = {"hq_rowblk_prob": ROWBLK_PROB, "hq_copy_item": COPY_ITEM, "hq_ge
                 "hq_applyq_prob": APPLYQ_PROB, "hq_svd_prob": SVD_PROB, "hq_slab": SLAB,
                 "hq_leaf_prob": LEAF_PROB}
 
-EXPORTS = ("hq_abi_version", "hq_device_check", "hq_gemm", "hq_gemm_skinny", "hq_concat", "hq_qr", "hq_applyq",
+EXPORTS = ("hq_abi_version", "hq_device_check", "hq_gemm", "hq_gemm_tiled", "hq_gemm_skinny", "hq_concat", "hq_qr", "hq_applyq",
            "hq_svd", "hq_leaf_gather", "hq_leaf_scatter", "hq_zero", "hq_power_step", "hq_copy",
            "hq_pack_offsets", "hq_rowblocks")
 
@@ -62,6 +62,7 @@ SIGNATURES = {
     "hq_abi_version": [],
     "hq_device_check": [],
     "hq_gemm": [_vp, _vp, _i, _vp, _vp, _i, _i, _vp],
+    "hq_gemm_tiled": [_vp, _vp, _i, _vp, _vp, _i, _i, _i, _vp],
     "hq_gemm_skinny": [_vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _vp],
     "hq_concat": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_qr": [_vp, _vp, _i, _vp, _i],

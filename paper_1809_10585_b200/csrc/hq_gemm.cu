@@ -7,12 +7,34 @@
 #include "hq_common.cuh"
 
 namespace {
-constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
+constexpr int NT = 256, BK = 16;
 
-__global__ void __launch_bounds__(NT) gemm_kernel(const hq_gemm_prob* __restrict__ probs,
-                                                  const hq_gemm_term* __restrict__ terms,
-                                                  const int* __restrict__ rank, int ksplit,
-                                                  const int* __restrict__ skip) {
+// async 8-byte copy with zero fill when !valid (src-size 0)
+__device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// FP64 tensor-core GEMM, BM x BN output tile per CTA, WM x WN warps (each a
+// (BM/WM) x (BN/WN) block of m8n8 tiles), k-tiles of BK staged in shared
+// memory with asynchronous copies, STAGES deep (the next STAGES-1 k-tiles are
+// in flight while the current one runs on mma.sync.m8n8k4).  Operands are staged in
+// their raw layout as op(A)[k][i], op(B)[k][j] with leading dims == 4 mod 16
+// (bank-conflict-free fragment fetches); masks and alpha are applied by the
+// thread that copied the element, before the barrier that publishes the tile.
+template <int BM, int BN, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* __restrict__ probs,
+                                                            const hq_gemm_term* __restrict__ terms,
+                                                            const int* __restrict__ rank, int ksplit,
+                                                            const int* __restrict__ skip) {
+  constexpr int NTH = WM * WN * 32;
+  constexpr int LDA = BM + 4, LDB = BN + 4;
+  constexpr int TM = BM / WM / 8, TN = BN / WN / 8;   // m8n8 tiles per warp
+  constexpr int EA = BM * BK / NTH, EB = BN * BK / NTH;  // staged elements per thread
   if (skip && *skip) return;
   const hq_gemm_prob P = probs[blockIdx.y];
   const int m = hq_dim(rank, P.m, P.m_ri), n = hq_dim(rank, P.n, P.n_ri);
@@ -24,90 +46,157 @@ __global__ void __launch_bounds__(NT) gemm_kernel(const hq_gemm_prob* __restrict
   // per-problem split: at least 8 k-tiles per slice (short-K problems of a
   // split launch keep one slice; the output was pre-zeroed either way)
   int ks = ksplit;
+  int nkt = 0;
+  for (int ti = 0; ti < P.nterm; ++ti)
+    nkt += (hq_dim(rank, terms[P.term0 + ti].k, terms[P.term0 + ti].k_ri) + BK - 1) / BK;
   if (ksplit > 1) {
-    int nkt = 0;
-    for (int ti = 0; ti < P.nterm; ++ti) {
-      const hq_gemm_term T = terms[P.term0 + ti];
-      nkt += (hq_dim(rank, T.k, T.k_ri) + BK - 1) / BK;
-    }
     ks = min(ksplit, max(1, nkt / 8));
     if ((int)blockIdx.z >= ks) return;
   }
 
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][BN + 1];
-  const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
-  double acc[4][4];
+  extern __shared__ __align__(16) double gsm[];
+  double (*As)[BK][LDA] = reinterpret_cast<double (*)[BK][LDA]>(gsm);
+  double (*Bs)[BK][LDB] = reinterpret_cast<double (*)[BK][LDB]>(gsm + STAGES * BK * LDA);
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int gq = lane >> 2, tq = lane & 3;
+  const int wm = wid % WM, wn = wid / WM;
+  double acc[TM][TN][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < TM; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int b = 0; b < TN; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  int gk = 0;  // global k-tile counter across terms (split-K striping)
-  for (int ti = 0; ti < P.nterm; ++ti) {
-    const hq_gemm_term T = terms[P.term0 + ti];
-    const int kd = hq_dim(rank, T.k, T.k_ri);
-    for (int k0 = 0; k0 < kd; k0 += BK, ++gk) {
-      if (ks > 1 && (gk % ks) != (int)blockIdx.z) continue;
-      // ---- A tile: op(A)(i, kk)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        int ii, kk;
-        if (T.ta == 0) { ii = t & 63; kk = (t >> 6) + 4 * r; }
-        else { kk = t & 15; ii = (t >> 4) + 16 * r; }
-        const int gi = i0 + ii, gkk = k0 + kk;
-        double v = 0.0;
-        if (gi < m && gkk < kd) {
-          if (T.ta == 0) v = hq_mask(T.a[gi + (size_t)gkk * T.lda], gi, gkk, T.mask_a);
-          else v = hq_mask(T.a[gkk + (size_t)gi * T.lda], gkk, gi, T.mask_a);
-        }
-        As[kk][ii] = v;
-      }
-      // ---- B tile: op(B)(kk, j)
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        int jj, kk;
-        if (T.tb == 0) { kk = t & 15; jj = (t >> 4) + 16 * r; }
-        else { jj = t & 63; kk = (t >> 6) + 4 * r; }
-        const int gj = j0 + jj, gkk = k0 + kk;
-        double v = 0.0;
-        if (gj < n && gkk < kd) {
-          if (T.tb == 0) v = hq_mask(T.b[gkk + (size_t)gj * T.ldb], gkk, gj, T.mask_b);
-          else v = hq_mask(T.b[gj + (size_t)gkk * T.ldb], gj, gkk, T.mask_b);
-        }
-        Bs[kk][jj] = v * T.alpha;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int kk = 0; kk < BK; ++kk) {
-        double av[4], bv[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) av[a] = As[kk][tx + 16 * a];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) bv[b] = Bs[kk][ty + 16 * b];
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-          for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
-      }
-      __syncthreads();
+  // flat sequence of this CTA's k-tiles: (term, k0)
+  int ti = 0, k0 = 0, gk = 0;
+  auto advance = [&](int& ti_, int& k0_, int& gk_) {
+    // move to the next k-tile of this slice (ti_ == nterm: none left)
+    for (;;) {
+      k0_ += BK;
+      if (ti_ >= P.nterm) return;
+      const int kd = hq_dim(rank, terms[P.term0 + ti_].k, terms[P.term0 + ti_].k_ri);
+      if (k0_ >= kd) { ++ti_; k0_ = -BK; continue; }
+      ++gk_;   // a real k-tile of the problem (split-K striping counter)
+      if (ks > 1 && (gk_ % ks) != (int)blockIdx.z) continue;
+      return;
     }
+  };
+  // position on the first k-tile of the slice
+  {
+    ti = 0; k0 = -BK; gk = -1;
+    advance(ti, k0, gk);
   }
-  // ---- epilogue
+  auto stage = [&](int buf, int ti_, int k0_) {
+    const hq_gemm_term T = terms[P.term0 + ti_];
+    const int kd = hq_dim(rank, T.k, T.k_ri);
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
-    const int gi = i0 + tx + 16 * a;
+    for (int e = 0; e < EA; ++e) {
+      const int idx = t + e * NTH;
+      int ii, kk;
+      if (T.ta == 0) { ii = idx % BM; kk = idx / BM; }
+      else { kk = idx % BK; ii = idx / BK; }
+      const int gi = i0 + ii, gkk = k0_ + kk;
+      const bool ok = gi < m && gkk < kd;
+      const double* src = T.ta == 0 ? T.a + (ok ? gi + (size_t)gkk * T.lda : 0)
+                                    : T.a + (ok ? gkk + (size_t)gi * T.lda : 0);
+      cp_async8_zfill(&As[buf][kk][ii], src, ok);
+    }
+#pragma unroll
+    for (int e = 0; e < EB; ++e) {
+      const int idx = t + e * NTH;
+      int jj, kk;
+      if (T.tb == 0) { kk = idx % BK; jj = idx / BK; }
+      else { jj = idx % BN; kk = idx / BN; }
+      const int gj = j0 + jj, gkk = k0_ + kk;
+      const bool ok = gj < n && gkk < kd;
+      const double* src = T.tb == 0 ? T.b + (ok ? gkk + (size_t)gj * T.ldb : 0)
+                                    : T.b + (ok ? gj + (size_t)gkk * T.ldb : 0);
+      cp_async8_zfill(&Bs[buf][kk][jj], src, ok);
+    }
+  };
+  // masks / alpha on the elements this thread staged (after they landed)
+  auto fixup = [&](int buf, int ti_, int k0_) {
+    const hq_gemm_term T = terms[P.term0 + ti_];
+    if (T.mask_a != 0) {
+#pragma unroll
+      for (int e = 0; e < EA; ++e) {
+        const int idx = t + e * NTH;
+        int ii, kk;
+        if (T.ta == 0) { ii = idx % BM; kk = idx / BM; }
+        else { kk = idx % BK; ii = idx / BK; }
+        const int gi = i0 + ii, gkk = k0_ + kk;
+        double& v = As[buf][kk][ii];
+        v = T.ta == 0 ? hq_mask(v, gi, gkk, T.mask_a) : hq_mask(v, gkk, gi, T.mask_a);
+      }
+    }
+    if (T.mask_b != 0 || T.alpha != 1.0) {
+#pragma unroll
+      for (int e = 0; e < EB; ++e) {
+        const int idx = t + e * NTH;
+        int jj, kk;
+        if (T.tb == 0) { kk = idx % BK; jj = idx / BK; }
+        else { jj = idx % BN; kk = idx / BN; }
+        const int gj = j0 + jj, gkk = k0_ + kk;
+        double& v = Bs[buf][kk][jj];
+        const double w = T.tb == 0 ? hq_mask(v, gkk, gj, T.mask_b) : hq_mask(v, gj, gkk, T.mask_b);
+        v = w * T.alpha;
+      }
+    }
+  };
+
+  // ring of STAGES buffers: tile s of the slice lives in buffer s % STAGES
+  int sti[STAGES], sk0[STAGES];
+  int pti = ti, pk0 = k0, pgk = gk;   // next tile to stage
+#pragma unroll
+  for (int q = 0; q < STAGES - 1; ++q) {
+    sti[q] = pti; sk0[q] = pk0;
+    if (pti < P.nterm) { stage(q, pti, pk0); advance(pti, pk0, pgk); }
+    cp_async_commit();
+  }
+  int buf = 0;
+  while (sti[buf] < P.nterm) {
+    // stage tile (current + STAGES-1) into the buffer freed last iteration
+    const int nb = (buf + STAGES - 1) % STAGES;
+    sti[nb] = pti; sk0[nb] = pk0;
+    if (pti < P.nterm) { stage(nb, pti, pk0); advance(pti, pk0, pgk); }
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    fixup(buf, sti[buf], sk0[buf]);
+    __syncthreads();
+#pragma unroll
+    for (int kq = 0; kq < BK; kq += 4) {
+      double av[TM], bv[TN];
+#pragma unroll
+      for (int a = 0; a < TM; ++a) av[a] = As[buf][kq + tq][(wm * TM + a) * 8 + gq];
+#pragma unroll
+      for (int b = 0; b < TN; ++b) bv[b] = Bs[buf][kq + tq][(wn * TN + b) * 8 + gq];
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) dmma884(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+    }
+    __syncthreads();   // this buffer is restaged next iteration
+    buf = (buf + 1) % STAGES;
+  }
+  cp_async_wait<0>();
+  // ---- epilogue: lane holds D[gq][2tq + {0,1}] of each m8n8 tile
+#pragma unroll
+  for (int a = 0; a < TM; ++a) {
+    const int gi = i0 + (wm * TM + a) * 8 + gq;
     if (gi >= m) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int gj = j0 + ty + 16 * b;
-      if (gj >= n) continue;
-      double* cp = P.c + gi + (size_t)gj * P.ldc;
-      if (ksplit > 1) atomicAdd(cp, acc[a][b]);
-      else *cp = (P.beta == 0.0) ? acc[a][b] : fma(P.beta, *cp, acc[a][b]);
+    for (int b = 0; b < TN; ++b) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gj = j0 + (wn * TN + b) * 8 + 2 * tq + h;
+        if (gj >= n) continue;
+        double* cp = P.c + gi + (size_t)gj * P.ldc;
+        if (ksplit > 1) atomicAdd(cp, acc[a][b][h]);
+        else *cp = (P.beta == 0.0) ? acc[a][b][h] : fma(P.beta, *cp, acc[a][b][h]);
+      }
     }
   }
 }
+
 // Skinny variant for outputs with few columns (n <= NC) and long K (the
 // power-iteration products: blocks^T X with 2 vectors, the 2x2 Gram): a
 // CTA owns a K-slice of one problem, its threads stride over k and keep an
@@ -259,12 +348,32 @@ extern "C" int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob
   return hq_err(cudaGetLastError());
 }
 
-extern "C" int hq_gemm(void* stream, const hq_gemm_prob* probs, int nprob,
-                       const hq_gemm_term* terms, int* rank, int tiles, int ksplit,
-                       const int* skip) {
+extern "C" int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob,
+                             const hq_gemm_term* terms, int* rank, int tiles, int ksplit, int tile,
+                             const int* skip) {
   if (nprob <= 0 || tiles <= 0) return 0;
   if (ksplit < 1) ksplit = 1;
   dim3 grid(tiles, nprob, ksplit);
-  gemm_kernel<<<grid, NT, 0, (cudaStream_t)stream>>>(probs, terms, rank, ksplit, skip);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (tile == 32) {
+    constexpr int S = 4, smem = S * BK * (36 + 36) * 8;
+    gemm_kernel<32, 32, 2, 2, S><<<grid, 128, smem, st>>>(probs, terms, rank, ksplit, skip);
+  } else {
+    constexpr int S = 3, smem = S * BK * (68 + 68) * 8;
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(gemm_kernel<64, 64, 2, 4, S>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return hq_err(e);
+      attr = true;
+    }
+    gemm_kernel<64, 64, 2, 4, S><<<grid, 256, smem, st>>>(probs, terms, rank, ksplit, skip);
+  }
   return hq_err(cudaGetLastError());
+}
+
+extern "C" int hq_gemm(void* stream, const hq_gemm_prob* probs, int nprob,
+                       const hq_gemm_term* terms, int* rank, int tiles, int ksplit,
+                       const int* skip) {
+  return hq_gemm_tiled(stream, probs, nprob, terms, rank, tiles, ksplit, 64, skip);
 }

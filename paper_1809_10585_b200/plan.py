@@ -290,6 +290,11 @@ class Builder:
         tiles = max(math.ceil(p[2].cap / GEMM_TILE) * math.ceil(p[3].cap / GEMM_TILE) for p in probs)
         if tiles <= 0:
             return
+        # few output tiles: 32 x 32 tiles put 4x the CTAs (SMs) on the product
+        tile = GEMM_TILE
+        if tiles * len(probs) * ksplit < 96:
+            tile = 32
+            tiles = max(math.ceil(p[2].cap / 32) * math.ceil(p[3].cap / 32) for p in probs)
         ncmax = max(p[3].cap for p in probs)
         mmax = max(p[2].cap for p in probs)
         kmax = max(max(t[8].cap for t in p[5]) for p in probs)
@@ -302,7 +307,7 @@ class Builder:
             # (only ever lowered: the caller zeroed C for ksplit > 1)
             ksplit = max(1, min(ksplit, kmax // 2048))
         self.op("gemm", probs, dict(tiles=tiles, ksplit=ksplit, skip=skip, skinny=skinny, ncmax=ncmax,
-                                    mode=mode, max_rows=mmax))
+                                    mode=mode, max_rows=mmax, tile=tile))
 
     def zero(self, regions):
         if regions:
@@ -1109,7 +1114,8 @@ class CompiledPlan:
                     rc = lib.hq_gemm_skinny(stream_handle, dp + o1, cnt, dp + o2, rk, ex["ksplit"], ex["ncmax"],
                                             ex["mode"], ex["max_rows"], skip)
                 else:
-                    rc = lib.hq_gemm(stream_handle, dp + o1, cnt, dp + o2, rk, ex["tiles"], ex["ksplit"], skip)
+                    rc = lib.hq_gemm_tiled(stream_handle, dp + o1, cnt, dp + o2, rk, ex["tiles"], ex["ksplit"],
+                                           ex.get("tile", 64), skip)
             elif kind == "zero":
                 rc = lib.hq_zero(stream_handle, dp + o1, cnt, ex["max_count"])
             elif kind == "concat":

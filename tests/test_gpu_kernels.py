@@ -32,9 +32,11 @@ def put(torch, arr):
     return torch.tensor(raw, device="cuda")
 
 
+@pytest.mark.parametrize("tile", [32, 64])
 @pytest.mark.parametrize("m,n,k,ta,tb", [(25, 3, 25, 0, 0), (25, 25, 6, 1, 0), (7, 33, 65, 0, 1),
-                                         (130, 70, 19, 1, 1), (1, 1, 1, 0, 0)])
-def test_gemm(dev, m, n, k, ta, tb):
+                                         (130, 70, 19, 1, 1), (1, 1, 1, 0, 0), (257, 129, 300, 0, 0),
+                                         (64, 64, 64, 1, 1)])
+def test_gemm(dev, m, n, k, ta, tb, tile):
     torch, lib = dev
     rng = np.random.default_rng(m * 100 + n)
     A = rng.standard_normal((k, m) if ta else (m, k))
@@ -47,11 +49,51 @@ def test_gemm(dev, m, n, k, ta, tb):
     probs = np.zeros(1, _abi.GEMM_PROB)
     probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 1, 0, 2.0)
     dt, dp = put(torch, terms), put(torch, probs)
-    tiles = -(-m // 64) * -(-n // 64)
-    assert lib.hq_gemm(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), tiles, 1, None) == 0
+    tiles = -(-m // tile) * -(-n // tile)
+    assert lib.hq_gemm_tiled(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), tiles, 1, tile, None) == 0
     torch.cuda.synchronize()
     ref = 2.0 * C - 0.5 * ((A.T if ta else A) @ (B.T if tb else B))
     assert np.allclose(back(dC, m, n), ref, atol=1e-12 * max(1, np.abs(ref).max()))
+
+
+@pytest.mark.parametrize("tile", [32, 64])
+@pytest.mark.parametrize("m,n,k,ta,tb,ks,masks", [(100, 70, 300, 0, 0, 1, (1, 0)), (33, 90, 257, 1, 0, 3, (2, 0)),
+                                                  (130, 20, 40, 0, 1, 1, (0, 1)), (64, 64, 512, 1, 1, 4, (0, 2))])
+def test_gemm_terms_masks(dev, m, n, k, ta, tb, ks, masks, tile):
+    """hq_gemm_tiled: two terms (k-tiles of both stream through one pipeline),
+    triangular masks, alpha, beta or atomic split-K into a zeroed C."""
+    torch, lib = dev
+    rng = np.random.default_rng(m + 3 * n + 7 * k)
+    A = rng.standard_normal((k, m) if ta else (m, k))
+    B = rng.standard_normal((n, k) if tb else (k, n))
+    A2 = rng.standard_normal((m, 21))
+    B2 = rng.standard_normal((21, n))
+    C = rng.standard_normal((m, n)) if ks == 1 else np.zeros((m, n))
+    dA, dB, dA2, dB2, dC = (colmajor(torch, x) for x in (A, B, A2, B2, C))
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    terms = np.zeros(2, _abi.GEMM_TERM)
+    terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, masks[0], masks[1], 0.75)
+    terms[1] = (dA2.data_ptr(), dB2.data_ptr(), m, 21, 0, 0, 21, -1, 0, 0, -1.0)
+    probs = np.zeros(1, _abi.GEMM_PROB)
+    beta = 0.5 if ks == 1 else 0.0
+    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta)
+    dt, dp = put(torch, terms), put(torch, probs)
+    tiles = -(-m // tile) * -(-n // tile)
+    assert lib.hq_gemm_tiled(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), tiles, ks, tile, None) == 0
+    torch.cuda.synchronize()
+
+    def mask(x, mk):
+        if mk == 1:
+            return np.triu(x)
+        if mk == 2:
+            y = np.tril(x, -1)
+            np.fill_diagonal(y, 1.0)
+            return y
+        return x
+    opA = (mask(A, masks[0])).T if ta else mask(A, masks[0])
+    opB = (mask(B, masks[1])).T if tb else mask(B, masks[1])
+    ref = beta * C + 0.75 * (opA @ opB) - A2 @ B2
+    assert np.allclose(back(dC, m, n), ref, atol=1e-11 * max(1, np.abs(ref).max()))
 
 
 @pytest.mark.parametrize("mode", [0, 1])
