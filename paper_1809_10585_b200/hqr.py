@@ -13,7 +13,10 @@ without a CUDA device or the library this raises.
 from __future__ import annotations
 
 import math
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
+from functools import lru_cache
 
 import numpy as np
 
@@ -50,9 +53,81 @@ def _start_vectors(n):
     return np.linalg.qr(x)[0]
 
 
+_POOL = None
+
+
+def _pool():
+    """Host worker threads for packing / assembling factor streams (numpy
+    copies release the GIL)."""
+    global _POOL
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)),
+                                   thread_name_prefix="hqb200-io")
+    return _POOL
+
+
+@lru_cache(maxsize=8)
+def _start_block(n):
+    x = _start_vectors(n) if n >= 2 else np.ones((1, 2))
+    x = np.asfortranarray(x)
+    x.flags.writeable = False
+    return x
+
+
+@lru_cache(maxsize=16)
+def _lower_mask(n):
+    m = np.tril(np.ones((n, n), dtype=bool), -1)
+    m.flags.writeable = False
+    return m
+
+
+_CPOOL = None
+
+
+def _fresh_copy(src, parts):
+    """np.array(src) with the copy (and the page faults of the fresh memory)
+    split over `parts` threads of a pool separate from the assembly workers."""
+    global _CPOOL
+    if parts <= 1 or src.size < (1 << 21):
+        return np.array(src)
+    if _CPOOL is None:
+        _CPOOL = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)),
+                                    thread_name_prefix="hqb200-copy")
+    dst = np.empty_like(src)
+    step = -(-src.size // parts)
+    fs = [_CPOOL.submit(np.copyto, dst[i:i + step], src[i:i + step]) for i in range(0, src.size, step)]
+    for f in fs:
+        f.result()
+    return dst
+
+
+def _copy_items(dst, items):
+    """items: (offset, rows, cols, src); writes src column-major at offset."""
+    for o, r, c, src in items:
+        np.copyto(dst[o:o + r * c].reshape((r, c), order="F"), src)
+
+
+def _split_even(items, weight, parts):
+    """Consecutive groups of roughly equal total weight."""
+    tot = sum(weight(i) for i in items)
+    groups, cur, acc = [], [], 0.0
+    for it in items:
+        cur.append(it)
+        acc += weight(it)
+        if acc >= tot / parts and len(groups) < parts - 1:
+            groups.append(cur)
+            cur, acc = [], 0.0
+    if cur:
+        groups.append(cur)
+    return groups
+
+
 class PlanIO:
     """Host side of a plan: packs inputs into the compact input stream and
-    assembles HodlrMatrix factors from the compact output stream (no CUDA)."""
+    assembles HodlrMatrix factors from the compact output stream (no CUDA).
+
+    Both streams are grouped by matrix (all items of matrix 0, then 1, ...);
+    item offsets are prefix sums of rows x (capacity or run-time rank)."""
 
     def __init__(self, tree: PartitionTree, batch: int = 1, eps: float = 1e-10,
                  absolute: bool = False, kcap: int = 512):
@@ -65,6 +140,13 @@ class PlanIO:
         self.rk = np.zeros(max(bld.slots.n, 1), np.int32)
         self.sc = np.zeros(max(2 * batch, 2))
         self.n_in = 0
+        self.in_ranges = [(0, 0)] * batch
+        oi = bld.out_items
+        self._o_rows = np.array([r for _, r, _ in oi], np.int64)
+        self._o_cap = np.array([c.cap for _, _, c in oi], np.int64)
+        self._o_ri = np.array([c.ri for _, _, c in oi], np.int64)
+        self._o_per_b = len(oi) // max(batch, 1)
+        self._o_key = [(buf.reg, buf.off) for buf, _, _ in oi]
 
     @staticmethod
     def _nodes(a: HodlrMatrix, t):
@@ -80,64 +162,116 @@ class PlanIO:
         walk(a, (0, 0))
         return out
 
-    def pack(self, mats):
-        """Input ranks -> rank table, factors -> compact input stream."""
+    def _sources(self, b, a):
+        """Rank-table entries and the input arrays of matrix b in stream order
+        (leaves, then per internal node a12.L, a12.R^T, a21.L, a21.R^T)."""
+        bld = self.builder
+        t, lay = bld.tree, bld.lay
+        if tuple(a.leaf_sizes()) != tuple(self.tree.leaf_sizes):
+            raise ValueError("matrix does not match the plan's partition tree")
+        nodes = self._nodes(a, t)
+        d = lay.m[b]
+        srcs = [nodes[lf].dense for lf in t.leaves((0, 0))]
+        for u in (t.internal_nodes((0, 0)) if t.L > 0 else []):
+            h = nodes[u]
+            kc = lay.kc[u]
+            for blk, slot in ((h.a12, "rA12"), (h.a21, "rA21")):
+                if blk.rank > kc:
+                    raise RankCapacityError(f"input block rank {blk.rank} exceeds capacity {kc}")
+                self.rk[d[slot][u]] = blk.rank
+            srcs += [h.a12.L, h.a12.R.T, h.a21.L, h.a21.R.T]
+        return srcs
+
+    def pack_async(self, mats):
+        """Fill the rank table, then copy every matrix's factors into the
+        compact input stream on the worker threads.  Returns one future per
+        matrix (its stream range is self.in_ranges[b])."""
         if len(mats) != self.B:
             raise ValueError(f"expected {self.B} matrices, got {len(mats)}")
         bld = self.builder
-        t, lay = bld.tree, bld.lay
-        rk = self.rk
-        rk[:] = 0
-        chunks = []
+        self.rk[:] = 0
+        n = bld.tree.n
+        x0 = _start_block(n)
+        per_mat, off = [], 0
         for b, a in enumerate(mats):
-            if tuple(a.leaf_sizes()) != tuple(self.tree.leaf_sizes):
-                raise ValueError("matrix does not match the plan's partition tree")
-            nodes = self._nodes(a, t)
-            d = lay.m[b]
-            for lf in t.leaves((0, 0)):
-                chunks.append(nodes[lf].dense.ravel(order="F"))
-            for u in (t.internal_nodes((0, 0)) if t.L > 0 else []):
-                h = nodes[u]
-                kc = lay.kc[u]
-                for blk, slot in ((h.a12, "rA12"), (h.a21, "rA21")):
-                    if blk.rank > kc:
-                        raise RankCapacityError(f"input block rank {blk.rank} exceeds capacity {kc}")
-                    rk[d[slot][u]] = blk.rank
-                chunks += [h.a12.L.ravel(order="F"), h.a12.R.T.ravel(order="F"),
-                           h.a21.L.ravel(order="F"), h.a21.R.T.ravel(order="F")]
-            n = t.n
-            x0 = _start_vectors(n) if n >= 2 else np.ones((1, 2))
+            srcs = self._sources(b, a)
+            o0 = off
+            items = []
+            for s in srcs:
+                r, c = s.shape
+                items.append((off, r, c, s))
+                off += r * c
+            self.in_ranges[b] = (o0, off)
+            per_mat.append(items)
             self.px[2 * n * b:2 * n * (b + 1)] = x0.ravel(order="F")
-        flat = np.concatenate(chunks) if chunks else np.zeros(0)
-        self.inbuf[:flat.size] = flat
-        self.n_in = flat.size
+        self.n_in = off
         sc = self.sc
         sc[:] = 0.0
         if self.absolute:
             sc[1::2] = self.eps
             for b in range(self.B):
-                rk[bld.power_done + b] = 1
-            rk[bld.all_done] = 1
+                self.rk[bld.power_done + b] = 1
+            self.rk[bld.all_done] = 1
+        pool = _pool()
+        nthr = pool._max_workers
+        futs = []
+        for items in per_mat:
+            groups = _split_even(items, lambda it: it[1] * it[2],
+                                 max(1, min(len(items), nthr // max(1, len(per_mat)))))
+            futs.append([pool.submit(_copy_items, self.inbuf, g) for g in groups])
+        return futs
 
-    def factors(self, b: int, out=None, rk=None) -> HodlrQRFactors:
-        """Assemble the HodlrMatrix factors of matrix b from the compact output."""
+    def pack(self, mats):
+        """Input ranks -> rank table, factors -> compact input stream."""
+        for fs in self.pack_async(mats):
+            for f in fs:
+                f.result()
+
+    def out_offsets(self, rk):
+        """Per-item offsets into the compact output stream for rank table rk;
+        returns (offsets[items + 1], per-item column counts)."""
+        ri = self._o_ri
+        cols = np.where(ri < 0, self._o_cap,
+                        np.minimum(np.maximum(rk[np.maximum(ri, 0)], 0), self._o_cap))
+        off = np.zeros(len(ri) + 1, np.int64)
+        np.cumsum(self._o_rows * cols, out=off[1:])
+        return off, cols
+
+    def out_range(self, b, offs):
+        i0 = b * self._o_per_b
+        return int(offs[0][i0]), int(offs[0][i0 + self._o_per_b])
+
+    def factors(self, b: int, out=None, rk=None, offs=None, copy=True, out_base=0) -> HodlrQRFactors:
+        """Assemble the HodlrMatrix factors of matrix b from the compact output
+        `out` (holding the stream from position out_base on).  With copy, its
+        range is first copied into fresh memory; the blocks are views of it."""
         bld = self.builder
         t = bld.tree
         d = bld.lay.m[b]
-        blocks, off = {}, 0
-        for (buf, rows, cols) in bld.out_items:
-            c = cols.cap if cols.ri < 0 else int(min(max(rk[cols.ri], 0), cols.cap))
-            blocks[(buf.reg, buf.off)] = out[off:off + rows * c].reshape((rows, c), order="F")
-            off += rows * c
-        get = lambda buf: blocks[(buf.reg, buf.off)].copy()
+        offs = self.out_offsets(rk) if offs is None else offs
+        off, cols = offs
+        i0 = b * self._o_per_b
+        lo, hi = int(off[i0]), int(off[i0 + self._o_per_b])
+        parts = max(1, (os.cpu_count() or 1) // max(1, self.B))
+        src = out[lo - out_base:hi - out_base]
+        base = _fresh_copy(src, parts) if copy else src
+        blocks = {}
+        for i in range(i0, i0 + self._o_per_b):
+            r, c = int(self._o_rows[i]), int(cols[i])
+            s = int(off[i]) - lo
+            blocks[self._o_key[i]] = base[s:s + r * c].reshape((r, c), order="F")
+        get = lambda buf: blocks[(buf.reg, buf.off)]
 
         def build(v, which):
             if t.is_leaf(v):
                 if which == "t":
-                    return HodlrMatrix(dense=np.triu(get(d["leafT"][v])), shape_tag=UPPER_TRIANGULAR)
+                    tl = get(d["leafT"][v])
+                    np.copyto(tl, 0.0, where=_lower_mask(tl.shape[0]))
+                    return HodlrMatrix(dense=tl, shape_tag=UPPER_TRIANGULAR)
                 full = get(d["leafA"][v])
                 if which == "r":
-                    return HodlrMatrix(dense=np.triu(full), shape_tag=UPPER_TRIANGULAR)
+                    np.copyto(full, 0.0, where=_lower_mask(full.shape[0]))
+                    return HodlrMatrix(dense=full, shape_tag=UPPER_TRIANGULAR)
                 y = np.tril(full, -1)
                 np.fill_diagonal(y, 1.0)
                 return HodlrMatrix(dense=y, shape_tag=UNIT_LOWER_TRIANGULAR)
@@ -154,7 +288,9 @@ class PlanIO:
                 a12 = LowRankBlock(get(d["A12U"][v]), get(d["A12V"][v]).T, True)
             return HodlrMatrix(a11=h1, a22=h2, a12=a12, a21=zero21, shape_tag=UPPER_TRIANGULAR)
 
-        return HodlrQRFactors(y=build((0, 0), "y"), t=build((0, 0), "t"), r=build((0, 0), "r"))
+        # Y first: it reads the strictly lower part of the leaves that R zeroes
+        y = build((0, 0), "y")
+        return HodlrQRFactors(y=y, t=build((0, 0), "t"), r=build((0, 0), "r"))
 
 
 class HQREngine(PlanIO):
@@ -275,20 +411,60 @@ class HQREngine(PlanIO):
             self.h_out[:self.n_out].copy_(self.d_out[:self.n_out], non_blocking=True)
         self.stream.synchronize()
 
-    def factors(self, b: int, out=None, rk=None) -> HodlrQRFactors:
-        return PlanIO.factors(self, b, self.outbuf if out is None else out,
-                              self.h_rk_out.numpy() if rk is None else rk)
+    def factors(self, b: int, out=None, rk=None, offs=None, copy=True) -> HodlrQRFactors:
+        rk = self.h_rk_out.numpy() if rk is None else rk
+        return PlanIO.factors(self, b, self.outbuf if out is None else out, rk, offs, copy)
 
     def norm_estimate(self, b: int = 0) -> float:
         """||A_b||_2 estimate of the last run (device power iteration)."""
         return float(self.plan.scal[2 * b].item())
 
     def factorize(self, mats):
-        self.pack(mats)
-        self.upload()
+        """pack (worker threads) -> H2D per matrix as its range is packed ->
+        graph replay -> rank table D2H -> per-matrix D2H of the compact factors,
+        each matrix assembled on a worker thread as soon as its copy lands."""
+        torch = self.torch
+        futs = self.pack_async(mats)
+        p = self.plan
+        with torch.cuda.stream(self.stream):
+            p.rank.copy_(self.h_rk, non_blocking=True)
+            p.scal.copy_(self.h_sc, non_blocking=True)
+            self.d_px.copy_(self.h_px, non_blocking=True)
+            for b, fs in enumerate(futs):
+                for f in fs:
+                    f.result()
+                lo, hi = self.in_ranges[b]
+                if hi > lo:
+                    self.d_in[lo:hi].copy_(self.h_in[lo:hi], non_blocking=True)
         self.execute()
-        self.download()
-        return [self.factors(b) for b in range(self.B)]
+        with torch.cuda.stream(self.stream):
+            self.h_tot.copy_(p.totals, non_blocking=True)
+            self.h_rk_out.copy_(p.rank, non_blocking=True)
+        self.stream.synchronize()
+        rk = self.h_rk_out.numpy().copy()
+        if int(rk[self.builder.flag_slot]) != 0:
+            raise RankCapacityError(f"a truncated rank exceeded the capacity kcap={self.kcap}; "
+                                    "retry with a larger kcap")
+        offs = self.out_offsets(rk)
+        self.n_out = int(offs[0][-1])
+        pool = _pool()
+        jobs = []
+        with torch.cuda.stream(self.stream):
+            for b in range(self.B):
+                # each matrix's factors land in their own pinned block (torch's
+                # caching host allocator recycles it once the caller drops them)
+                lo, hi = self.out_range(b, offs)
+                hb = torch.empty(max(hi - lo, 1), dtype=torch.float64, pin_memory=True)
+                if hi > lo:
+                    hb[:hi - lo].copy_(self.d_out[lo:hi], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(self.stream)
+                jobs.append(pool.submit(self._assemble, b, ev, rk, offs, hb, lo))
+        return [j.result() for j in jobs]
+
+    def _assemble(self, b, ev, rk, offs, hb, lo):
+        ev.synchronize()
+        return PlanIO.factors(self, b, hb.numpy(), rk, offs, False, lo)
 
 
 _ENGINES: dict = {}
