@@ -144,12 +144,14 @@ typedef struct hq_leaf_prob {
 
 /* one column-major 2D copy dst(rows x cols) = src; cols from the rank table
    when cols_ri >= 0 (used to restore inputs and to compact the factors for
-   the single device->host copy) */
+   the single device->host copy).  mode 0 copies; mode 1 writes the upper
+   triangle (zeros below the diagonal: R and T leaves); mode 2 the unit lower
+   triangle (ones on the diagonal, zeros above: Y leaves) */
 typedef struct hq_copy_item {
   const double* src;
   double* dst;
   int32_t rows, cols, cols_ri, lds, ldd;
-  int32_t pad_;
+  int32_t mode;
 } hq_copy_item;
 
 /* TSQR row blocks of a tall factor stack W (rows_total x K, chunks of ch rows

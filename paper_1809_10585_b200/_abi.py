@@ -42,7 +42,7 @@ LEAF_PROB = np.dtype([("leaf", P), ("panel", P), ("nl", I), ("ldp", I), ("slab0"
                       ("nslab", I), ("m_ri", I), ("pad_", I)], align=True)
 
 COPY_ITEM = np.dtype([("src", P), ("dst", P), ("rows", I), ("cols", I), ("cols_ri", I),
-                      ("lds", I), ("ldd", I), ("pad_", I)], align=True)
+                      ("lds", I), ("ldd", I), ("mode", I)], align=True)
 
 ROWBLK_PROB = np.dtype([("s", P), ("w", P), ("lds", I), ("ldw", I), ("ch", I), ("rows_total", I),
                         ("k", I), ("k_ri", I), ("ncol", I), ("ncol_ri", I), ("ms_ri", I),

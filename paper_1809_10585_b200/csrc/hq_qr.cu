@@ -787,7 +787,10 @@ __global__ void copy_kernel(const hq_copy_item* __restrict__ items, const int* _
   const size_t n = (size_t)it.rows * cols;
   for (size_t e = threadIdx.x; e < n; e += blockDim.x) {
     const int i = (int)(e % it.rows), j = (int)(e / it.rows);
-    it.dst[i + (size_t)j * it.ldd] = it.src[i + (size_t)j * it.lds];
+    double v = it.src[i + (size_t)j * it.lds];
+    if (it.mode == 1 && i > j) v = 0.0;
+    if (it.mode == 2) v = i < j ? 0.0 : (i == j ? 1.0 : v);
+    it.dst[i + (size_t)j * it.ldd] = v;
   }
 }
 

@@ -74,13 +74,6 @@ def _start_block(n):
     return x
 
 
-@lru_cache(maxsize=16)
-def _lower_mask(n):
-    m = np.tril(np.ones((n, n), dtype=bool), -1)
-    m.flags.writeable = False
-    return m
-
-
 _CPOOL = None
 
 
@@ -142,11 +135,11 @@ class PlanIO:
         self.n_in = 0
         self.in_ranges = [(0, 0)] * batch
         oi = bld.out_items
-        self._o_rows = np.array([r for _, r, _ in oi], np.int64)
-        self._o_cap = np.array([c.cap for _, _, c in oi], np.int64)
-        self._o_ri = np.array([c.ri for _, _, c in oi], np.int64)
+        self._o_rows = np.array([r for _, r, _, _ in oi], np.int64)
+        self._o_cap = np.array([c.cap for _, _, c, _ in oi], np.int64)
+        self._o_ri = np.array([c.ri for _, _, c, _ in oi], np.int64)
         self._o_per_b = len(oi) // max(batch, 1)
-        self._o_key = [(buf.reg, buf.off) for buf, _, _ in oi]
+        self._o_key = [(buf.reg, buf.off, mode) for buf, _, _, mode in oi]
 
     @staticmethod
     def _nodes(a: HodlrMatrix, t):
@@ -260,21 +253,16 @@ class PlanIO:
             r, c = int(self._o_rows[i]), int(cols[i])
             s = int(off[i]) - lo
             blocks[self._o_key[i]] = base[s:s + r * c].reshape((r, c), order="F")
-        get = lambda buf: blocks[(buf.reg, buf.off)]
+        get = lambda buf, mode=0: blocks[(buf.reg, buf.off, mode)]
 
         def build(v, which):
             if t.is_leaf(v):
+                # leaves arrive masked (R, T upper; Y unit lower: hq_copy modes)
                 if which == "t":
-                    tl = get(d["leafT"][v])
-                    np.copyto(tl, 0.0, where=_lower_mask(tl.shape[0]))
-                    return HodlrMatrix(dense=tl, shape_tag=UPPER_TRIANGULAR)
-                full = get(d["leafA"][v])
+                    return HodlrMatrix(dense=get(d["leafT"][v], 1), shape_tag=UPPER_TRIANGULAR)
                 if which == "r":
-                    np.copyto(full, 0.0, where=_lower_mask(full.shape[0]))
-                    return HodlrMatrix(dense=full, shape_tag=UPPER_TRIANGULAR)
-                y = np.tril(full, -1)
-                np.fill_diagonal(y, 1.0)
-                return HodlrMatrix(dense=y, shape_tag=UNIT_LOWER_TRIANGULAR)
+                    return HodlrMatrix(dense=get(d["leafA"][v], 1), shape_tag=UPPER_TRIANGULAR)
+                return HodlrMatrix(dense=get(d["leafA"][v], 2), shape_tag=UNIT_LOWER_TRIANGULAR)
             c1, c2 = t.children(v)
             m1, m2 = t.size[c1], t.size[c2]
             h1, h2 = build(c1, which), build(c2, which)
@@ -288,9 +276,7 @@ class PlanIO:
                 a12 = LowRankBlock(get(d["A12U"][v]), get(d["A12V"][v]).T, True)
             return HodlrMatrix(a11=h1, a22=h2, a12=a12, a21=zero21, shape_tag=UPPER_TRIANGULAR)
 
-        # Y first: it reads the strictly lower part of the leaves that R zeroes
-        y = build((0, 0), "y")
-        return HodlrQRFactors(y=y, t=build((0, 0), "t"), r=build((0, 0), "r"))
+        return HodlrQRFactors(y=build((0, 0), "y"), t=build((0, 0), "t"), r=build((0, 0), "r"))
 
 
 class HQREngine(PlanIO):
@@ -324,6 +310,7 @@ class HQREngine(PlanIO):
         self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
         # side streams pay off when a launch leaves most SMs idle (few matrices)
         self.multi_stream = batch <= 8
+        self._pins = []
         self._evs = []
 
     def upload(self):
@@ -454,13 +441,27 @@ class HQREngine(PlanIO):
                 # each matrix's factors land in their own pinned block (torch's
                 # caching host allocator recycles it once the caller drops them)
                 lo, hi = self.out_range(b, offs)
-                hb = torch.empty(max(hi - lo, 1), dtype=torch.float64, pin_memory=True)
+                hb = self._pinned_block(hi - lo)
                 if hi > lo:
                     hb[:hi - lo].copy_(self.d_out[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(self.stream)
                 jobs.append(pool.submit(self._assemble, b, ev, rk, offs, hb, lo))
         return [j.result() for j in jobs]
+
+    def _pinned_block(self, size):
+        """A pinned host block of >= size doubles that no live result views.
+        Returned factors are numpy views whose base is the block's tensor, so
+        a block is free again once only the pool references its storage."""
+        pool = self._pins
+        use = getattr(self.torch._C, "_storage_Use_Count", None)
+        for blk in pool:
+            if use is not None and blk.numel() >= size and use(blk.untyped_storage()._cdata) <= 2:
+                return blk
+        blk = self.torch.empty(max(size + size // 8, 1), dtype=self.torch.float64, pin_memory=True)
+        if len(pool) < 4 * self.B + 4:
+            pool.append(blk)
+        return blk
 
     def _assemble(self, b, ev, rk, offs, hb, lo):
         ev.synchronize()

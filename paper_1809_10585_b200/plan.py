@@ -235,18 +235,20 @@ class Builder:
             for lf in t.leaves((0, 0)):
                 nl = t.size[lf]
                 ins.append((d["leafA"][lf], nl, Dim(nl)))
-                outs.append((d["leafA"][lf], nl, Dim(nl)))
-                outs.append((d["leafT"][lf], nl, Dim(nl)))
+                # R (upper), Y (unit lower) and T (upper) leaves, masked on the device
+                outs.append((d["leafA"][lf], nl, Dim(nl), 1))
+                outs.append((d["leafA"][lf], nl, Dim(nl), 2))
+                outs.append((d["leafT"][lf], nl, Dim(nl), 1))
             for u in (t.internal_nodes((0, 0)) if t.L > 0 else []):
                 c1, c2 = t.children(u)
                 m1, m2, kc = t.size[c1], t.size[c2], lay.kc[u]
                 ins += [(d["A12U"][u], m1, Dim(kc, d["rA12"][u])), (d["A12V"][u], m2, Dim(kc, d["rA12"][u])),
                         (d["A21U"][u], m2, Dim(kc, d["rA21"][u])), (d["A21V"][u], m1, Dim(kc, d["rA21"][u]))]
-                outs += [(d["A12U"][u], m1, Dim(kc, d["rA12"][u])), (d["A12V"][u], m2, Dim(kc, d["rA12"][u])),
-                         (d["A21U"][u], m2, Dim(kc, d["rA21"][u])), (d["YV21"][u], m1, Dim(kc, d["rA21"][u])),
-                         (d["T12U"][u], m1, Dim(kc, d["rT12"][u])), (d["T12V"][u], m2, Dim(kc, d["rT12"][u]))]
+                outs += [(d["A12U"][u], m1, Dim(kc, d["rA12"][u]), 0), (d["A12V"][u], m2, Dim(kc, d["rA12"][u]), 0),
+                         (d["A21U"][u], m2, Dim(kc, d["rA21"][u]), 0), (d["YV21"][u], m1, Dim(kc, d["rA21"][u]), 0),
+                         (d["T12U"][u], m1, Dim(kc, d["rT12"][u]), 0), (d["T12V"][u], m2, Dim(kc, d["rT12"][u]), 0)]
         self.bumps[R_IN].alloc(sum(r * c.cap for _, r, c in ins))
-        self.bumps[R_OUT].alloc(sum(r * c.cap for _, r, c in outs))
+        self.bumps[R_OUT].alloc(sum(r * c.cap for _, r, c, _ in outs))
         return ins, outs
 
     # ------------------------------------------------------------ primitives
@@ -912,11 +914,11 @@ def op_resources(builder, kind, probs, extra):
     elif kind == "pack_copy":
         if extra["which"] == 1:
             rd(Buf(R_IN, 0))
-            for (buf, rows, cols) in probs:
+            for (buf, rows, cols, *_) in probs:
                 wr(buf), slot(cols)
         else:
             W.add(("m", R_OUT, 0)), W.add(("totals",))
-            for (buf, rows, cols) in probs:
+            for (buf, rows, cols, *_) in probs:
                 rd(buf), slot(cols)
     else:
         raise ValueError(kind)
@@ -1053,11 +1055,11 @@ class CompiledPlan:
                 self.launch.append(("rowblk", put(pa), None, len(probs), extra))
             elif kind == "pack_copy":
                 it = np.zeros(len(probs), _abi.COPY_ITEM)
-                for i, (buf, rows, cols) in enumerate(probs):
+                for i, (buf, rows, cols, *mode) in enumerate(probs):
                     if extra["which"] == 1:
                         it[i] = (0, A(buf), rows, cols.cap, cols.ri, rows, rows, 0)
                     else:
-                        it[i] = (A(buf), 0, rows, cols.cap, cols.ri, rows, rows, 0)
+                        it[i] = (A(buf), 0, rows, cols.cap, cols.ri, rows, rows, mode[0] if mode else 0)
                 self.launch.append(("pack_copy", put(it), None, len(probs),
                                     dict(extra, base_ptr=A(extra["base"]))))
             else:
@@ -1192,7 +1194,7 @@ def op_bytes(kind, probs, rk):
             k = sum(_dv(d, rk) for _, _, d, _ in pieces)
             by += 8.0 * rows * k * (3 if dst2 is not None else 2)
     elif kind == "pack_copy":
-        for (buf, rows, cols) in probs:
+        for (buf, rows, cols, *_) in probs:
             by += 16.0 * rows * _dv(cols, rk)
     elif kind in ("leaf_gather", "leaf_scatter"):
         for (leaf, panel, nl, ldp, slabs, mri) in probs:

@@ -279,7 +279,13 @@ class Emu:
                 src = self.mat(it["src"], it["lds"], rows, cols)
                 dst = self.mat(base + 8 * off, rows, rows, cols)
             if rows and cols:
-                dst[:] = np.array(src)
+                v = np.array(src)
+                if it["mode"] == 1:
+                    v = np.triu(v)
+                elif it["mode"] == 2:
+                    v = np.tril(v, -1)
+                    np.fill_diagonal(v, 1.0)
+                dst[:] = v
             off += rows * cols
         self.plan.totals.numpy()[ex["total"]] = off
 

@@ -32,7 +32,7 @@ def sketch_matrix(n):
 
 
 def main():
-    which = [int(a) for a in sys.argv[1:]] or [0, 1, 2, 4]
+    which = [int(a) for a in sys.argv[1:]] or [0, 1, 2, 3, 4]
     for ci in which:
         c = gen.CONFIGS[ci]
         t0 = time.time()

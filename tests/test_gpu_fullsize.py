@@ -44,7 +44,7 @@ def estimate_metrics(a, f):
     return e_orth, e_acc
 
 
-@pytest.mark.parametrize("ci", [0, 1, 2, 4])
+@pytest.mark.parametrize("ci", [0, 1, 2, 3, 4])
 def test_full_config_vs_reference(ci):
     import torch
     if not torch.cuda.is_available():
