@@ -256,7 +256,7 @@ def main():
     per_step = total_batch if total_batch > 1 else ws * len(mats)
     value = per_step * args.steps / (ms / 1e3)
     # ---- end-to-end through the public API with host buffers
-    for _ in range(2):  # untimed warm-up: host worker pools and pinned result blocks
+    for _ in range(3):  # untimed warm-up: host worker pools and pinned result blocks
         f = eng.factorize(mats)
     barrier()
     torch.cuda.synchronize()
@@ -306,7 +306,10 @@ def main():
     if not args.no_instrument and rank == 0:
         per = instrument(eng, torch)
         tot = sum(v[0] for v in per.values())
-        kinds = {k: {"ms": v[0], "launches": v[1], "share": v[0] / tot} for k, v in per.items()}
+        kinds = {k: {"ms": v[0], "launches": v[1], "share": v[0] / tot,
+                     "gflop": acc.get(k, {}).get("flops", 0.0) / 1e9,
+                     "tflops": acc.get(k, {}).get("flops", 0.0) / max(v[0], 1e-9) / 1e9,
+                     "gbytes": acc.get(k, {}).get("bytes", 0.0) / 1e9} for k, v in per.items()}
         top = max((k for k in per if acc.get(k, {}).get("flops", 0) > 0), key=lambda k: per[k][0])
         peak_fp64 = 37.16e12  # self-measured DMMA m8n8k4 FP64 (profiles/r01_fp64_peak.txt)
         ach = acc[top]["flops"] / (per[top][0] / 1e3)

@@ -54,6 +54,7 @@ def _start_vectors(n):
 
 
 _POOL = None
+_now = __import__("time").perf_counter
 
 
 def _pool():
@@ -276,7 +277,11 @@ class PlanIO:
                 a12 = LowRankBlock(get(d["A12U"][v]), get(d["A12V"][v]).T, True)
             return HodlrMatrix(a11=h1, a22=h2, a12=a12, a21=zero21, shape_tag=UPPER_TRIANGULAR)
 
-        return HodlrQRFactors(y=build((0, 0), "y"), t=build((0, 0), "t"), r=build((0, 0), "r"))
+        out = HodlrQRFactors(y=build((0, 0), "y"), t=build((0, 0), "t"), r=build((0, 0), "r"))
+        # `build` is a self-referencing closure (a reference cycle): drop the
+        # block views it can reach so only the returned factors hold the memory
+        blocks.clear()
+        return out
 
 
 class HQREngine(PlanIO):
@@ -411,6 +416,7 @@ class HQREngine(PlanIO):
         graph replay -> rank table D2H -> per-matrix D2H of the compact factors,
         each matrix assembled on a worker thread as soon as its copy lands."""
         torch = self.torch
+        tr = [("start", _now())]
         futs = self.pack_async(mats)
         p = self.plan
         with torch.cuda.stream(self.stream):
@@ -423,42 +429,63 @@ class HQREngine(PlanIO):
                 lo, hi = self.in_ranges[b]
                 if hi > lo:
                     self.d_in[lo:hi].copy_(self.h_in[lo:hi], non_blocking=True)
+        tr.append(("packed", _now()))
         self.execute()
+        tr.append(("replay_enqueued", _now()))
         with torch.cuda.stream(self.stream):
             self.h_tot.copy_(p.totals, non_blocking=True)
             self.h_rk_out.copy_(p.rank, non_blocking=True)
         self.stream.synchronize()
+        tr.append(("device_done", _now()))
         rk = self.h_rk_out.numpy().copy()
         if int(rk[self.builder.flag_slot]) != 0:
             raise RankCapacityError(f"a truncated rank exceeded the capacity kcap={self.kcap}; "
                                     "retry with a larger kcap")
         offs = self.out_offsets(rk)
         self.n_out = int(offs[0][-1])
+        tr.append(("offsets", _now()))
         pool = _pool()
         jobs = []
         with torch.cuda.stream(self.stream):
+            taken = []
             for b in range(self.B):
-                # each matrix's factors land in their own pinned block (torch's
-                # caching host allocator recycles it once the caller drops them)
+                # each matrix's factors land in their own pinned block, recycled
+                # once the caller drops every factor that views it
                 lo, hi = self.out_range(b, offs)
-                hb = self._pinned_block(hi - lo)
+                hb = self._pinned_block(hi - lo, taken)
+                taken.append(hb)
+                tr.append((f"pinned{b}", _now()))
                 if hi > lo:
                     hb[:hi - lo].copy_(self.d_out[lo:hi], non_blocking=True)
+                tr.append((f"d2h{b}", _now()))
                 ev = torch.cuda.Event()
                 ev.record(self.stream)
                 jobs.append(pool.submit(self._assemble, b, ev, rk, offs, hb, lo))
-        return [j.result() for j in jobs]
+        tr.append(("d2h_enqueued", _now()))
+        out = [j.result() for j in jobs]
+        tr.append(("assembled", _now()))
+        self.last_trace = {k: (t - tr[0][1]) * 1e3 for k, t in tr}
+        return out
 
-    def _pinned_block(self, size):
+    def _pinned_block(self, size, taken=()):
         """A pinned host block of >= size doubles that no live result views.
         Returned factors are numpy views whose base is the block's tensor, so
         a block is free again once only the pool references its storage."""
         pool = self._pins
         use = getattr(self.torch._C, "_storage_Use_Count", None)
-        for blk in pool:
-            if use is not None and blk.numel() >= size and use(blk.untyped_storage()._cdata) <= 2:
-                return blk
-        blk = self.torch.empty(max(size + size // 8, 1), dtype=self.torch.float64, pin_memory=True)
+        best = None
+        if use is not None:
+            for blk in pool:
+                if (blk.numel() >= size and not any(blk is t for t in taken)
+                        and use(blk.untyped_storage()._cdata) <= 2):
+                    if best is None or blk.numel() < best.numel():
+                        best = blk
+        if best is not None:
+            return best
+        self.pin_allocs = getattr(self, "pin_allocs", 0) + 1
+        quantum = 1 << 20  # 8 MB granules, +25 % headroom for rank variation
+        blk = self.torch.empty(-(-max(size + size // 4, 1) // quantum) * quantum, dtype=self.torch.float64,
+                               pin_memory=True)
         if len(pool) < 4 * self.B + 4:
             pool.append(blk)
         return blk

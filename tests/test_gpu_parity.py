@@ -64,3 +64,25 @@ def test_gpu_matches_oracle(hqr_gpu, name):
     # truncation ranks agree with the oracle's to within a few
     for mine, ref in ((f.y, y), (f.t, t), (f.r, r)):
         assert abs(stats(mine)["max_offdiag_rank"] - stats(ref)["max_offdiag_rank"]) <= 4
+
+
+def test_gpu_batched_results_independent_and_persistent(hqr_gpu):
+    """A batch factorization returns each matrix's own factors (equal to the
+    single-matrix run), and results stay valid across later calls that reuse
+    the engine's pinned result blocks."""
+    from paper_1809_10585_b200 import hqr_batched
+    mats = [gen.gen_random_hodlr(512, 64, 8, 8.0, seed=s) for s in range(4)]
+    fb = hqr_batched(mats, 1e-10)
+    snap = [to_dense(f.r).copy() for f in fb]
+    for a, f, rd in zip(mats, fb, snap):
+        single = to_dense(hqr_gpu(a, 1e-10).r)
+        assert np.linalg.norm(rd - single) <= 1e-12 * np.linalg.norm(single)
+    for _ in range(3):  # later calls must not overwrite live results
+        other = hqr_batched([gen.gen_random_hodlr(512, 64, 8, 8.0, seed=s + 10) for s in range(4)], 1e-10)
+        del other
+        fb2 = hqr_batched(mats, 1e-10)
+        for f, rd in zip(fb, snap):
+            assert np.array_equal(to_dense(f.r), rd)
+        del fb2
+    for i in range(3):
+        assert np.linalg.norm(snap[i] - snap[i + 1]) > 1e-3 * np.linalg.norm(snap[i])

@@ -13,17 +13,20 @@ for _ in range(2):
     f = eng.factorize(mats)
 del f
 T = {}
-def tick(k, t0):
-    torch.cuda.synchronize(); T[k] = T.get(k, 0) + time.perf_counter() - t0; return time.perf_counter()
-for _ in range(3):
+def tick(k, t0, sync=True):
+    if sync: torch.cuda.synchronize()
+    T[k] = T.get(k, 0) + time.perf_counter() - t0; return time.perf_counter()
+R = 3
+for _ in range(R):
     t = time.perf_counter()
     eng.pack(mats); t = tick("pack", t)
     eng.upload(); t = tick("h2d", t)
-    eng.execute(); t = tick("replay", t)
+    eng.execute(); t = tick("replay_enqueue", t, False)
+    torch.cuda.synchronize(); t = tick("replay_wait", t)
     eng.download(); t = tick("d2h_staging", t)
     fs = [eng.factors(b) for b in range(B)]; t = tick("assemble_serial", t)
     del fs
-    f = eng.factorize(mats); t = tick("factorize_total", t)
+    f = eng.factorize(mats); t = tick("factorize_total", t); print({k: round(v, 1) for k, v in eng.last_trace.items()}, "pin_allocs", getattr(eng, "pin_allocs", 0))
     del f
-print({k: round(v / 3 * 1e3, 1) for k, v in T.items()}, "ms; bytes in %.0f MB out %.0f MB" %
+print(f"B={B}", {k: round(v / R * 1e3, 1) for k, v in T.items()}, "ms; bytes in %.0f MB out %.0f MB" %
       (eng.h2d_bytes() / 1e6, eng.d2h_bytes() / 1e6))
