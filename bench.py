@@ -4,7 +4,7 @@
 Workload (BASELINE.json metric "at n=16384"): config 2, the ill-conditioned
 HODLR matrix, n = 16384, leaf 256, off-diagonal rank 16, A = D B with
 D = diag(logspace(0,-14,n)) permuted, tol 1e-10 relative.  One step = one
-batch of 8 independent such matrices (seeds 8*rank .. 8*rank+7) factorized
+batch of 32 independent such matrices (seeds 32*rank .. 32*rank+31) factorized
 by one graph replay: power iteration for ||A||_2, the unrolled Algorithm 2,
 compaction of Y, T, R.  `latency_ms_single_matrix` reports one matrix alone.
 
@@ -50,9 +50,11 @@ def parse():
     p.add_argument("--config", type=int, default=2)
     p.add_argument("--n", type=int, default=None, help="override n (smoke runs)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--kcap", type=int, default=None,
+                   help="rank capacity of the plan (overflow raises RankCapacityError, never truncates)")
     p.add_argument("--no-instrument", action="store_true")
     p.add_argument("--batch", type=int, default=None,
-                   help="matrices per step per GPU (config 2 default 8; config 4 is the fixed 64-batch)")
+                   help="matrices per step per GPU (config 2 default 32; config 4 is the fixed 64-batch)")
     return p.parse_args()
 
 
@@ -215,12 +217,15 @@ def main():
         seeds = shard_seeds(total_batch, ws, rank)
         scaling = "strong"
     else:
-        per = args.batch or 8
+        per = args.batch or 32
         seeds = list(range(rank * per, (rank + 1) * per))
         scaling = "weak"
     mats = [gen_config(args.config, seed=s, n=n) for s in seeds]
     a = mats[0]
-    eng = HQREngine(a.tree(), len(mats), cfg["tol"], device=f"cuda:{local}")
+    # rank capacity 256 (max rank seen on this workload: 158); an overflow
+    # raises RankCapacityError, it never truncates
+    kcap = args.kcap or (256 if total_batch == 1 else 512)
+    eng = HQREngine(a.tree(), len(mats), cfg["tol"], kcap=kcap, device=f"cuda:{local}")
     eng.pack(mats)
     eng.upload()
     eng.snapshot_device_input()
@@ -279,14 +284,15 @@ def main():
             "data": "synthetic (seeded generator of BASELINE config; seeds " +
                     ("0..%d sharded over ranks)" % (total_batch - 1) if total_batch > 1 else "= rank)"),
             "config": config_dict(args.config, n, {"parallelism": f"independent matrices x{ws}",
-                                                    "matrices_per_step_per_gpu": len(mats)}),
+                                                    "matrices_per_step_per_gpu": len(mats),
+                                                    "kcap": kcap}),
             "e2e": e2e, "gpu_launches": eng.plan.n_launch * args.steps,
             "fp64_gflops_effective": flops / (ms_step / 1e3) / 1e9,
             "algorithmic_gflop_per_step": flops / 1e9,
             "norm_estimate": eng.norm_estimate(0), "max_ranks": ranks, "clocks": clk}
     if rank == 0 and len(mats) > 1:
         # single-matrix latency (batch 1 plan, graph replay, input resident)
-        e1 = HQREngine(a.tree(), 1, cfg["tol"], device=f"cuda:{local}")
+        e1 = HQREngine(a.tree(), 1, cfg["tol"], kcap=kcap, device=f"cuda:{local}")
         e1.pack([a])
         e1.upload()
         e1.snapshot_device_input()

@@ -199,6 +199,7 @@ class PlanIO:
             per_mat.append(items)
             self.px[2 * n * b:2 * n * (b + 1)] = x0.ravel(order="F")
         self.n_in = off
+        self._ensure_inbuf(off)
         sc = self.sc
         sc[:] = 0.0
         if self.absolute:
@@ -214,6 +215,10 @@ class PlanIO:
                                  max(1, min(len(items), nthr // max(1, len(per_mat)))))
             futs.append([pool.submit(_copy_items, self.inbuf, g) for g in groups])
         return futs
+
+    def _ensure_inbuf(self, n):
+        """The compact input stream buffer (capacity-sized, lazily mapped)."""
+        return self.inbuf
 
     def pack(self, mats):
         """Input ranks -> rank table, factors -> compact input stream."""
@@ -295,17 +300,19 @@ class HQREngine(PlanIO):
         self.device = torch.device(device if device is not None else "cuda")
         self.plan = CompiledPlan(self.builder, self.device)
         pin = lambda a: torch.from_numpy(a).pin_memory()
-        self.h_in, self.h_rk, self.h_sc, self.h_px = pin(self.inbuf), pin(self.rk), pin(self.sc), pin(self.px)
-        self.inbuf, self.rk, self.sc, self.px = (self.h_in.numpy(), self.h_rk.numpy(), self.h_sc.numpy(),
-                                                 self.h_px.numpy())
-        self.h_out = pin(self.outbuf)
-        self.outbuf = self.h_out.numpy()
+        self.h_rk, self.h_sc, self.h_px = pin(self.rk), pin(self.sc), pin(self.px)
+        self.rk, self.sc, self.px = self.h_rk.numpy(), self.h_sc.numpy(), self.h_px.numpy()
+        # pinned host staging sized to the actual streams (the device regions
+        # are capacity-sized): grown on demand
+        in_cap, out_cap = self.inbuf.size, self.outbuf.size
+        self.h_in = self.h_out = None
+        self.inbuf = self.outbuf = None
         self.h_rk_out = torch.zeros_like(self.h_rk).pin_memory()
         self.h_tot = torch.zeros(2, dtype=torch.int64).pin_memory()
         p = self.plan
         ib, ob = p.bases[R_IN], p.bases[R_OUT]
-        self.d_in = p.arena[ib:ib + self.inbuf.size]
-        self.d_out = p.arena[ob:ob + self.outbuf.size]
+        self.d_in = p.arena[ib:ib + in_cap]
+        self.d_out = p.arena[ob:ob + out_cap]
         pxo = p.bases[R_PERSIST] + self.builder.PX.off
         self.d_px = p.arena[pxo:pxo + self.px.size]
         self.n_out = 0
@@ -314,9 +321,23 @@ class HQREngine(PlanIO):
         self.stream = torch.cuda.Stream(device=self.device)
         self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
         # side streams pay off when a launch leaves most SMs idle (few matrices)
-        self.multi_stream = batch <= 8
+        self.multi_stream = True
+        ms = os.environ.get("HQB200_MULTISTREAM")
+        if ms is not None:
+            self.multi_stream = ms not in ("0", "")
         self._pins = []
         self._evs = []
+
+    def _pinned_staging(self, cur, n):
+        if cur is not None and cur.numel() >= n:
+            return cur
+        return self.torch.empty(max(n + n // 4, 1), dtype=self.torch.float64, pin_memory=True)
+
+    def _ensure_inbuf(self, n):
+        h = self._pinned_staging(self.h_in, n)
+        if h is not self.h_in:
+            self.h_in, self.inbuf = h, h.numpy()
+        return self.inbuf
 
     def upload(self):
         """H2D of the compact input stream, the rank table and the scalars."""
@@ -399,6 +420,9 @@ class HQREngine(PlanIO):
             raise RankCapacityError(f"a truncated rank exceeded the capacity kcap={self.kcap}; "
                                     "retry with a larger kcap")
         self.n_out = int(self.h_tot.numpy()[1])
+        h = self._pinned_staging(self.h_out, self.n_out)
+        if h is not self.h_out:
+            self.h_out, self.outbuf = h, h.numpy()
         with self.torch.cuda.stream(self.stream):
             self.h_out[:self.n_out].copy_(self.d_out[:self.n_out], non_blocking=True)
         self.stream.synchronize()

@@ -118,3 +118,17 @@ if detail:
     print(f"on-path {detail} by (nprob, m64, k16, extra):")
     for k, (tm, c) in sorted(dd.items(), key=lambda x: -x[1][0])[:30]:
         print(f"    {str(k):40s} {c:4d} ops {tm:8.2f} ms  avg {1000 * tm / c:7.1f} us")
+if detail == "gemm":
+    from paper_1809_10585_b200.plan import op_flops
+    allc = collections.defaultdict(lambda: [0.0, 0, 0.0])
+    for i, (kind, probs, ex) in enumerate(ops):
+        if kind != "gemm" or not probs:
+            continue
+        mm = max(_dv(p[2], rk) for p in probs); nn = max(_dv(p[3], rk) for p in probs)
+        kk = max(sum(_dv(t[8], rk) for t in p[5]) for p in probs)
+        key = (len(probs), ex.get("ksplit"), ex.get("tile"), "m%d" % (1 << max(0, (mm - 1)).bit_length()),
+               "n%d" % (1 << max(0, (nn - 1)).bit_length()), "k%d" % (1 << max(0, (kk - 1)).bit_length()))
+        allc[key][0] += times[i]; allc[key][1] += 1; allc[key][2] += op_flops(kind, probs, rk)
+    print("all gemm ops by (nprob, ksplit, tile, m, n, sum k) pow2 classes:")
+    for k, (tm, c, fl) in sorted(allc.items(), key=lambda x: -x[1][0])[:30]:
+        print(f"    {str(k):56s} {c:4d} ops {tm:8.2f} ms  avg {1000 * tm / c:7.1f} us  {fl / max(tm, 1e-9) / 1e9:6.2f} TF/s")
