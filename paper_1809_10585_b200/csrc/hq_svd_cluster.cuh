@@ -316,8 +316,6 @@ __global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* 
     if (cr == 0 && t == 0) rank[P.rank_ri] = 0;
     return;
   }
-  // the plan sizes clusters from capacities; a core that fits one SM with one
-  // pass of pairs per round runs on CTA 0 alone (no exchange rounds)
   // the plan sizes clusters from capacities; the run-time core decides: one
   // SM when it fits with few pairs per round (no exchange rounds), the
   // cluster when its blocks fit the cluster's shared memory, else CTA 0 alone

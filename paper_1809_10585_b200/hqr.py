@@ -23,7 +23,7 @@ import numpy as np
 from . import _abi
 from .hodlr import (GENERAL, UNIT_LOWER_TRIANGULAR, UPPER_TRIANGULAR, HodlrMatrix, LowRankBlock,
                     PartitionTree)
-from .plan import R_IN, R_OUT, R_PERSIST, Builder, CompiledPlan
+from .plan import R_IN, R_OUT, R_PERSIST, Builder, CompiledPlan, retune_clusters
 
 
 class RankCapacityError(RuntimeError):
@@ -322,11 +322,23 @@ class HQREngine(PlanIO):
         self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
         # side streams pay off when a launch leaves most SMs idle (few matrices)
         self.multi_stream = True
+        self.autotune = os.environ.get("HQB200_AUTOTUNE", "1") not in ("0", "")
+        self._tuned = False
         ms = os.environ.get("HQB200_MULTISTREAM")
         if ms is not None:
             self.multi_stream = ms not in ("0", "")
         self._pins = []
         self._evs = []
+
+    def _retune(self, rk):
+        """After the first run, size the Jacobi clusters from the actual core
+        sizes (the plan only knows capacities); the next execute() captures
+        a new graph."""
+        if self._tuned or not self.autotune:
+            return
+        self._tuned = True
+        if retune_clusters(self.builder, rk):
+            self.graph = None
 
     def _pinned_staging(self, cur, n):
         if cur is not None and cur.numel() >= n:
@@ -419,6 +431,7 @@ class HQREngine(PlanIO):
         if int(rk[self.builder.flag_slot]) != 0:
             raise RankCapacityError(f"a truncated rank exceeded the capacity kcap={self.kcap}; "
                                     "retry with a larger kcap")
+        self._retune(rk.copy())
         self.n_out = int(self.h_tot.numpy()[1])
         h = self._pinned_staging(self.h_out, self.n_out)
         if h is not self.h_out:
@@ -467,6 +480,7 @@ class HQREngine(PlanIO):
                                     "retry with a larger kcap")
         offs = self.out_offsets(rk)
         self.n_out = int(offs[0][-1])
+        self._retune(rk)
         tr.append(("offsets", _now()))
         pool = _pool()
         jobs = []

@@ -822,6 +822,60 @@ def svd_cluster(svd_probs):
     return dict(cluster=8, max_m=mmax)
 
 
+SVD_C_SMEM_DOUBLES, SVD_C_MAX_BS = 22528, 64   # hq_svd_cluster.cuh C_SMEM_DOUBLES / C_MAX_BS
+
+
+def _svd_fits(G, m, n):
+    """The cluster kernel's own test (hq_svd_cluster.cuh): G CTAs hold the
+    core in 2G column blocks, two buffer sets."""
+    if G == 1:
+        return (m + 1) // 2 * 2 * n <= SVD_SMEM_DOUBLES
+    bs = -(-n // (2 * G))
+    return m <= 512 and 4 * bs * ((m + 1) // 2 * 2) <= SVD_C_SMEM_DOUBLES and bs <= SVD_C_MAX_BS
+
+
+def svd_cluster_runtime(nprob, m, n, sms=148):
+    """Cluster size for a Jacobi launch whose largest core is m x n (run-time
+    sizes, e.g. from a previous run of the plan): the smallest cluster whose
+    shared memory holds the core (a core that spills to the global-memory
+    path is 4-6x slower), widened while the launch still fits one wave."""
+    if n <= 0 or m <= 0:
+        return 1
+    if _svd_fits(1, m, n) and (n + 1) // 2 <= SVD_SINGLE_MAX_PAIRS:
+        return 1
+    fit = [G for G in (2, 4, 8) if _svd_fits(G, m, n)]
+    if not fit:
+        return 1
+    G = fit[0]
+    while G < 8 and nprob * 2 * G <= sms:
+        G *= 2
+    return G
+
+
+def retune_clusters(builder, rk, margin=1.1):
+    """Re-pick every Jacobi launch's cluster size from the core sizes of a
+    finished run (rank table rk) with some headroom; the launch records share
+    the ops' extra dicts.  Returns the number of launches changed (the caller
+    re-captures its graph)."""
+    changed = 0
+    for kind, probs, extra in builder.ops:
+        if kind != "svd" or not probs:
+            continue
+        mm = nn = 0
+        for p in probs:
+            m, n = _dv(p[5], rk), _dv(p[6], rk)
+            if p[12]:
+                n = min(n, m)
+            mm, nn = max(mm, m), max(nn, n)
+        m2 = min(int(mm * margin) + 1, p[5].cap) if mm else 0
+        n2 = min(int(nn * margin) + 1, m2) if nn else 0
+        G = svd_cluster_runtime(len(probs), m2, n2)
+        if G != extra.get("cluster", 1):
+            extra["cluster"] = G
+            changed += 1
+    return changed
+
+
 def _addr(buf, bases, base_ptr):
     if buf is None:
         return 0
