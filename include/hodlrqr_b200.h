@@ -185,7 +185,10 @@ int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob, const hq_g
    blocks^T X, Gram and leaf products).  mode 0: grid (ksplit, nprob), K split
    evenly over CTAs, with ksplit > 1 C must be zero on entry (atomic
    accumulation); mode 1: one thread per output row (max_rows bounds m),
-   ksplit ignored */
+   ksplit ignored; mode 2: 64 output rows per CTA (max_rows bounds m), each
+   term read coalesced in its own layout (rows across lanes for op(A) = A,
+   k across lanes for op(A) = A^T), K split into at most ksplit slices of
+   >= 512 (C zeroed by the caller when ksplit > 1) */
 int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
                    int* rank, int ksplit, int ncmax, int mode, int max_rows, const int* skip);
 int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_piece* pieces,

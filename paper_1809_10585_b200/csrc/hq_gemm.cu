@@ -325,6 +325,168 @@ __global__ void __launch_bounds__(NT) gemm_rows_kernel(const hq_gemm_prob* __res
     __syncthreads();
   }
 }
+// Streaming product for outputs of at most NC columns (the power iteration's
+// HODLR x 2 vectors, arith.py:35-64 on a 2-column block): HBM-bound, so each
+// term is read in its own coalesced pattern.  A CTA owns GV_ROWS output rows
+// of one problem (blockIdx.x) and a K-slice (blockIdx.z):
+//   op(A) = A   (ta = 0, column-major m x k): thread (row r, slice s) walks
+//               k = s, s + 4, ...; a warp load covers 32 consecutive rows;
+//   op(A) = A^T (ta = 1): row r of op(A) is a contiguous column of A: work
+//               items (row, k-lane-group) spread over the 8 warps, lanes along
+//               k, warp-shuffle reduction, shared-memory accumulation.
+// B (k x NC) is tiny and read through the cache.  K-split slices add into C
+// atomically (the caller zeroed C).
+constexpr int GV_ROWS = 64, GV_U = 8, GV_RQ = GV_ROWS / (NT / 32);
+template <int NC>
+__global__ void __launch_bounds__(NT, 2) gemv_kernel(const hq_gemm_prob* __restrict__ probs,
+                                                  const hq_gemm_term* __restrict__ terms,
+                                                  const int* __restrict__ rank, int ksplit,
+                                                  const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  const hq_gemm_prob P = probs[blockIdx.y];
+  const int m = hq_dim(rank, P.m, P.m_ri), n = hq_dim(rank, P.n, P.n_ri);
+  const int i0 = blockIdx.x * GV_ROWS;
+  if (m <= 0 || n <= 0 || i0 >= m) return;
+  const int nr = min(GV_ROWS, m - i0);
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int z = blockIdx.z;
+  __shared__ double part[NT / GV_ROWS][GV_ROWS][NC];
+  __shared__ double dotr[GV_ROWS][NC];
+  for (int e = t; e < GV_ROWS * NC; e += NT) dotr[e / NC][e % NC] = 0.0;
+  __syncthreads();
+  const int r = t % GV_ROWS, sl = t / GV_ROWS;
+  constexpr int NSL = NT / GV_ROWS;
+  double acc[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) acc[j] = 0.0;
+  // per-problem K split: slices of >= 512 k (the launch's ksplit bounds it)
+  int ktot = 0;
+  for (int ti = 0; ti < P.nterm; ++ti) ktot += hq_dim(rank, terms[P.term0 + ti].k, terms[P.term0 + ti].k_ri);
+  const int ks = min(ksplit, max(1, ktot / 512));
+  if (z >= ks) return;
+  // warps per A^T row: spread few rows over all warps
+  int wpr = 1;
+  while (wpr < 8 && nr * wpr * 2 <= 8) wpr *= 2;
+  for (int ti = 0; ti < P.nterm; ++ti) {
+    const hq_gemm_term T = terms[P.term0 + ti];
+    const int kd = hq_dim(rank, T.k, T.k_ri);
+    const int kb = (int)(((long long)kd * z) / ks), ke = (int)(((long long)kd * (z + 1)) / ks);
+    if (kb >= ke) continue;
+    // B element (k, j) = T.b[k * sbk + j * sbj]; columns past n read column 0
+    // (their sums are never stored)
+    const size_t sbk = T.tb == 0 ? 1 : (size_t)T.ldb, sbj = T.tb == 0 ? (size_t)T.ldb : 1;
+    size_t bj[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) bj[j] = (j < n ? j : 0) * sbj;
+    const bool plain = T.mask_a == 0 && T.mask_b == 0;
+    auto bval = [&](int k, int j) -> double {
+      const int jj = j < n ? j : 0;
+      return hq_mask(T.b[(size_t)k * sbk + bj[j]], T.tb == 0 ? k : jj, T.tb == 0 ? jj : k, T.mask_b);
+    };
+    if (T.ta == 0) {
+      if (r < nr) {
+        const int gi = i0 + r;
+        const double* ap = T.a + gi;
+        double tacc[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) tacc[j] = 0.0;
+        if (plain) {
+          // branch-free body: GV_U loads of A (and of B) issued before use
+          int k = kb + sl;
+          for (; k + (GV_U - 1) * NSL < ke; k += GV_U * NSL) {
+            double a[GV_U], b[GV_U][NC];
+#pragma unroll
+            for (int u = 0; u < GV_U; ++u) {
+              a[u] = __ldg(ap + (size_t)(k + u * NSL) * T.lda);
+#pragma unroll
+              for (int j = 0; j < NC; ++j) b[u][j] = __ldg(T.b + (size_t)(k + u * NSL) * sbk + bj[j]);
+            }
+#pragma unroll
+            for (int u = 0; u < GV_U; ++u)
+#pragma unroll
+              for (int j = 0; j < NC; ++j) tacc[j] = fma(a[u], b[u][j], tacc[j]);
+          }
+          for (; k < ke; k += NSL) {
+            const double a = __ldg(ap + (size_t)k * T.lda);
+#pragma unroll
+            for (int j = 0; j < NC; ++j) tacc[j] = fma(a, __ldg(T.b + (size_t)k * sbk + bj[j]), tacc[j]);
+          }
+        } else {
+          for (int k = kb + sl; k < ke; k += NSL) {
+            const double a = hq_mask(ap[(size_t)k * T.lda], gi, k, T.mask_a);
+#pragma unroll
+            for (int j = 0; j < NC; ++j) tacc[j] = fma(a, bval(k, j), tacc[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[j] = fma(T.alpha, tacc[j], acc[j]);
+      }
+    } else {
+      // warp w owns rows rr = w / wpr + (8 / wpr) q of this block and the
+      // k-lane-group w % wpr: all its rows advance together, so every k
+      // step issues one load per row (independent) plus the B loads
+      const int sub = wid % wpr, ngrp = (NT / 32) / wpr, r0 = wid / wpr;
+      const int st = 32 * wpr;
+      double d[GV_RQ][NC];
+#pragma unroll
+      for (int q = 0; q < GV_RQ; ++q)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) d[q][j] = 0.0;
+      // rows past nr re-read row r0 (their sums are dropped)
+      const double* ap0 = T.a + (size_t)(i0 + r0) * T.lda;
+      const size_t rstep = (size_t)ngrp * T.lda;
+      const int nq = r0 < nr ? (nr - 1 - r0) / ngrp + 1 : 0;   // valid rows of this warp
+      bool rv[GV_RQ];
+#pragma unroll
+      for (int q = 0; q < GV_RQ; ++q) rv[q] = q < nq;
+      if (plain) {
+        for (int k = kb + sub * 32 + lane; k < ke; k += st) {
+          double b[NC], a[GV_RQ];
+#pragma unroll
+          for (int j = 0; j < NC; ++j) b[j] = __ldg(T.b + (size_t)k * sbk + bj[j]);
+#pragma unroll
+          for (int q = 0; q < GV_RQ; ++q) a[q] = __ldg(ap0 + (rv[q] ? q * rstep : 0) + k);
+#pragma unroll
+          for (int q = 0; q < GV_RQ; ++q)
+#pragma unroll
+            for (int j = 0; j < NC; ++j) d[q][j] = fma(a[q], b[j], d[q][j]);
+        }
+      } else {
+        for (int k = kb + sub * 32 + lane; k < ke; k += st) {
+#pragma unroll
+          for (int q = 0; q < GV_RQ; ++q) {
+            if (!rv[q]) continue;
+            const double a = hq_mask(ap0[q * rstep + k], k, i0 + r0 + ngrp * q, T.mask_a);
+#pragma unroll
+            for (int j = 0; j < NC; ++j) d[q][j] = fma(a, bval(k, j), d[q][j]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < GV_RQ; ++q) {
+        if (!rv[q]) continue;   // warp-uniform
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const double v = warp_sum(d[q][j]);
+          if (lane == 0) atomicAdd(&dotr[r0 + ngrp * q][j], T.alpha * v);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NC; ++j) part[sl][r][j] = acc[j];
+  __syncthreads();
+  for (int e = t; e < nr * NC; e += NT) {
+    const int rr = e / NC, j = e % NC;
+    if (j >= n) continue;
+    double v = dotr[rr][j];
+#pragma unroll
+    for (int q = 0; q < NSL; ++q) v += part[q][rr][j];
+    double* cp = P.c + (i0 + rr) + (size_t)j * P.ldc;
+    if (ksplit > 1) atomicAdd(cp, v);
+    else *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
+  }
+}
 }  // namespace
 
 // skinny products (n <= 4 output columns).  mode 0: grid (ksplit, nprob),
@@ -336,6 +498,12 @@ extern "C" int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob
   if (nprob <= 0) return 0;
   if (ksplit < 1) ksplit = 1;
   cudaStream_t st = (cudaStream_t)stream;
+  if (mode == 2) {
+    dim3 grid((max_rows + GV_ROWS - 1) / GV_ROWS, nprob, ksplit);
+    if (ncmax <= 2) gemv_kernel<2><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+    else gemv_kernel<4><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+    return hq_err(cudaGetLastError());
+  }
   if (mode == 1) {
     dim3 grid((max_rows + 31) / 32, nprob);
     if (ncmax <= 2) gemm_rows_kernel<2><<<grid, NT, 0, st>>>(probs, terms, rank, skip);

@@ -303,7 +303,9 @@ class Builder:
         # outputs of <= 4 columns (power iteration): the skinny kernels --
         # threads along K for long K, one thread per output row otherwise
         skinny = ncmax <= SKINNY_MAX_COLS
-        mode = 0 if (kmax >= 1024 or mmax <= 64) else 1
+        # skinny products stream their operands (mode 2: coalesced per term
+        # layout, per-problem K slices); modes 0/1 remain in the ABI
+        mode = 2
         if skinny and mode == 0 and ksplit > 1:
             # a K-slice of >= 8 k per thread amortizes the CTA reduction
             # (only ever lowered: the caller zeroed C for ksplit > 1)
@@ -360,10 +362,21 @@ class Builder:
                         kmax = max(kmax, ncols)
                     p1.append((buf, kc, Dim(kc, R[u]), Dim(ncap, nris[b]), 0.0, [term]))
                     zeros.append((buf, kc * ncap))
-        ksplit = 1
-        if kmax >= 1024:
-            ksplit = min(32, kmax // 256)   # per problem the kernel uses <= nktiles/8 slices
-        if p1:
+        if p1 and ncap <= SKINNY_MAX_COLS:
+            # streaming V^T X products: one launch per block size (tree level)
+            # with its own K split, so no launch carries empty slices
+            groups = {}
+            for prob, z in zip(p1, zeros):
+                groups.setdefault(prob[5][0][8].cap, []).append((prob, z))
+            for kk in sorted(groups, reverse=True):
+                ks = max(1, min(32, kk // 512))
+                if ks > 1:
+                    self.zero([z for _, z in groups[kk]])
+                self.gemm([pr for pr, _ in groups[kk]], skip=skip, ksplit=ks)
+        elif p1:
+            ksplit = 1
+            if kmax >= 1024:
+                ksplit = min(32, kmax // 256)   # per problem the kernel uses <= nktiles/8 slices
             if ksplit > 1:
                 self.zero(zeros)
             self.gemm(p1, skip=skip, ksplit=ksplit)

@@ -96,7 +96,7 @@ def test_gemm_terms_masks(dev, m, n, k, ta, tb, ks, masks, tile):
     assert np.allclose(back(dC, m, n), ref, atol=1e-11 * max(1, np.abs(ref).max()))
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
 @pytest.mark.parametrize("m,n,k,ta,tb,ks,masks", [(16, 2, 8192, 1, 0, 32, (0, 0)), (2, 2, 5000, 1, 0, 19, (0, 0)),
                                                   (256, 2, 256, 0, 0, 1, (1, 0)), (37, 3, 300, 1, 1, 1, (2, 0)),
                                                   (70, 4, 900, 0, 1, 4, (0, 0)), (5, 1, 3, 1, 0, 1, (0, 0)),
