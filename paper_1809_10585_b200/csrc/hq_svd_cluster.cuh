@@ -330,12 +330,19 @@ __global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* 
   }
   CSmem& S = *reinterpret_cast<CSmem*>(smem_raw);
   // lane-group shape from the pairs per CTA (bs) and the rows (m)
+  // (rows per lane E sized to m: lanes past the column end only waste issue
+  // slots on the latency-bound rounds)
   if (bs <= 16 || m > 256) {
     if (m <= 128) svd_cluster_body<G, 32, 4>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 192) svd_cluster_body<G, 32, 6>(P, rank, m, n, thr, S, cluster);
     else if (m <= 256) svd_cluster_body<G, 32, 8>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 384) svd_cluster_body<G, 32, 12>(P, rank, m, n, thr, S, cluster);
     else svd_cluster_body<G, 32, 16>(P, rank, m, n, thr, S, cluster);
   } else if (bs <= 32 || m > 128) {
     if (m <= 128) svd_cluster_body<G, 16, 8>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 160) svd_cluster_body<G, 16, 10>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 192) svd_cluster_body<G, 16, 12>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 224) svd_cluster_body<G, 16, 14>(P, rank, m, n, thr, S, cluster);
     else svd_cluster_body<G, 16, 16>(P, rank, m, n, thr, S, cluster);
   } else {
     if (m <= 64) svd_cluster_body<G, 8, 8>(P, rank, m, n, thr, S, cluster);

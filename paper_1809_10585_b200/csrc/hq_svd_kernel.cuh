@@ -46,6 +46,18 @@ __device__ __forceinline__ double rsqrt_approx(double x) {
 // accurate, so t is formed from the hardware reciprocal / reciprocal-sqrt
 // approximations (~2^-22 relative: at most one extra sweep); only c is
 // computed to full FP64 accuracy by the caller.
+// c = (1 + t^2)^(-1/2) to full FP64 accuracy: hardware reciprocal square
+// root (~2^-22) refined by two Newton steps (quadratic: ~2^-44, ~2^-88),
+// shorter than the library rsqrt's generic path
+__device__ __forceinline__ double jacobi_cos(double tt) {
+  const double w = fma(tt, tt, 1.0);
+  double y = rsqrt_approx(w);
+  const double hw = 0.5 * w;
+  y = y * fma(-hw * y, y, 1.5);
+  y = y * fma(-hw * y, y, 1.5);
+  return y;
+}
+
 __device__ __forceinline__ double jacobi_tan(double a, double b, double g) {
   const double d = b - a;
   const double h = fabs(d) * (0.5 * rcp_approx(fabs(g)));
@@ -94,7 +106,7 @@ __device__ __forceinline__ bool jacobi_pair(double (&xp)[E], double* cx, double*
   const bool rot = work && g != 0.0 && g * g > tol2 * (a * b);
   if (rot) {
     const double tt = jacobi_tan(a, b, g);
-    const double c = rsqrt(fma(tt, tt, 1.0)), sn = c * tt;
+    const double c = jacobi_cos(tt), sn = c * tt;
     double2* sink = trash + (threadIdx.x & 31);
 #pragma unroll
     for (int e = 0; e < E / 2; ++e) {
@@ -230,7 +242,7 @@ __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, doubl
           const bool rot = work && g != 0.0 && g * g > tol2 * (a * b);
           if (rot) {
             const double tt = jacobi_tan(a, b, g);
-            const double c = rsqrt(fma(tt, tt, 1.0)), sn = c * tt;
+            const double c = jacobi_cos(tt), sn = c * tt;
 #pragma unroll
             for (int e = 0; e < E; ++e) {
               const int i = gl + e * LP;
