@@ -1,0 +1,53 @@
+"""Summarise an ncu --set full report: key SOL / occupancy / stall metrics,
+per-launch DRAM traffic, and the stall mix of the SASS source page."""
+import csv, subprocess, sys
+
+
+def page(rep, name, extra=()):
+    out = subprocess.run(["ncu", "-i", rep, "--page", name, "--csv", *extra], capture_output=True, text=True).stdout
+    return list(csv.reader(out.splitlines()))
+
+
+def summary(rep):
+    rows = page(rep, "details")
+    h = rows[0]
+    si, mi, vi, ui = (h.index(k) for k in ("Section Name", "Metric Name", "Metric Value", "Metric Unit"))
+    want = ["Duration", "Elapsed Cycles", "SM Active Cycles", "Executed Ipc Active", "Issue Slots Busy",
+            "DRAM Throughput", "L1/TEX Hit Rate", "L2 Hit Rate", "Warp Cycles Per Issued Instruction",
+            "Registers Per Thread", "Grid Size", "Block Size", "Cluster Size", "Achieved Occupancy",
+            "Dynamic Shared Memory Per Block", "Compute (SM) Throughput", "Memory Throughput"]
+    out = ["kernel: " + rows[1][h.index("Kernel Name")]]
+    seen = set()
+    for r in rows[1:]:
+        if r[mi] in want and (r[si], r[mi]) not in seen:
+            seen.add((r[si], r[mi]))
+            out.append(f"  {r[si][:30]:30s} {r[mi]:38s} {r[vi]:>14s} {r[ui]}")
+    raw = page(rep, "raw")
+    rh = raw[0]
+    row = raw[2] if len(raw) > 2 else raw[1]
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
+              "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+              "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+              "sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active"):
+        if k in rh:
+            out.append(f"  {k:70s} {row[rh.index(k)]} {raw[1][rh.index(k)]}")
+    src = page(rep, "source", ("--print-source", "sass"))
+    for hi, r in enumerate(src):
+        if "Source" in r and len(r) > 5:
+            break
+    sh = src[hi]
+    data = src[hi + 1:]
+    if "Warp Stall Sampling (All Samples)" in sh:
+        si2 = sh.index("Warp Stall Sampling (All Samples)")
+        cols = [c for c in sh if c.startswith("stall_") and "Not Issued" not in c]
+        tot = sum(float(r[si2] or 0) for r in data) or 1.0
+        agg = {c: sum(float(r[sh.index(c)] or 0) for r in data) for c in cols}
+        out.append("  stall mix (% of samples): " + ", ".join(
+            f"{k[6:]} {100 * v / tot:.1f}" for k, v in sorted(agg.items(), key=lambda x: -x[1])[:8]))
+    return "\n".join(out)
+
+
+if __name__ == "__main__":
+    for rep in sys.argv[1:]:
+        print(summary(rep))
+        print()
