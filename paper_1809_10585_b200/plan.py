@@ -492,12 +492,12 @@ class Builder:
             gm_v.append((V, ldv, Dim(n), Dim(cap, p["rank_ri"]), 0.0,
                          [(WRc, n, 0, 0, Mm, kcap, 0, 0, Dim(kcap, kL), 1.0)]))
         self.op("concat", cat, dict(max_rows=maxrows))
-        self.op("qr", qr)
+        self.op("qr", qr, dict(role="stack"))
         if stack:
             self.op("rowblk", stack, dict(max_chunks=maxch))
-            self.op("qr", qrs)
+            self.op("qr", qrs, dict(role="tsqr"))
         self.gemm(gm_c)
-        self.op("qr", qrc)
+        self.op("qr", qrc, dict(role="core"))
         self.op("svd", svd, svd_cluster(svd))
         self.op("applyq", apq, dict(max_cols=max(p[10].cap for p in apq)))
         if unstack:
@@ -602,7 +602,7 @@ class Builder:
                         m_ri))
             qr.append((panel, tau, tp, d["leafT"][v], mcap, nl, Dim(mcap, m_ri), Dim(nl)))
         self.op("leaf_gather", gat, dict(max_nl=nl))
-        self.op("qr", qr)
+        self.op("qr", qr, dict(role="leaf"))
         self.op("leaf_scatter", gat, dict(max_nl=nl))
 
     def s_phase(self, v):
@@ -1007,6 +1007,13 @@ def schedule(builder):
                 deps.add(last_w[r])
         for r in Ws:
             deps.update(readers.get(r, ()))
+        if kind == "pack_copy" and extra.get("which") == 0:
+            # the output compaction joins every lane: its region may alias
+            # scratch of the side lanes (CompiledPlan), so all of them finish first
+            last_in_lane = {}
+            for j, lj in enumerate(lanes):
+                last_in_lane[lj] = j
+            deps.update(last_in_lane.values())
         per_lane = {}
         for d in deps:
             if lanes[d] != ln:
@@ -1032,10 +1039,18 @@ class CompiledPlan:
         self.device = device
         sizes = {r: bp.peak for r, bp in builder.bumps.items()}
         self.region_sizes = sizes
+        # the compact output stream is written by the last op only (which joins
+        # every lane): it shares the largest scratch region that can hold it
+        scratch = [r for r in sizes if r not in (R_PERSIST, R_IN, R_OUT, R_SHARED) and sizes[r] >= sizes.get(R_OUT, 0)]
+        self.out_alias = max(scratch, key=lambda r: sizes[r]) if scratch and sizes.get(R_OUT, 0) > 0 else None
         bases, acc = {}, 0
         for r in sorted(sizes):
+            if r == R_OUT and self.out_alias is not None:
+                continue
             bases[r] = acc
             acc += (sizes[r] + 63) // 64 * 64
+        if self.out_alias is not None:
+            bases[R_OUT] = bases[self.out_alias]
         self.total_doubles = acc
         self.arena = torch.zeros(max(acc, 1), dtype=torch.float64, device=device)
         self.rank = torch.zeros(max(builder.slots.n, 1), dtype=torch.int32, device=device)

@@ -11,7 +11,7 @@ B = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 c = gen.CONFIGS[ci]
 mats = [gen.gen_config(ci, seed=s, n=n) for s in range(B)]
 a = mats[0]
-eng = HQREngine(a.tree(), B, c["tol"], use_graph=False)
+eng = HQREngine(a.tree(), B, c["tol"], kcap=256 if B > 1 else 512, use_graph=False)
 eng.factorize(mats)
 rk = eng.h_rk_out.numpy()
 plan = eng.plan
@@ -132,3 +132,14 @@ if detail == "gemm":
     print("all gemm ops by (nprob, ksplit, tile, m, n, sum k) pow2 classes:")
     for k, (tm, c, fl) in sorted(allc.items(), key=lambda x: -x[1][0])[:30]:
         print(f"    {str(k):56s} {c:4d} ops {tm:8.2f} ms  avg {1000 * tm / c:7.1f} us  {fl / max(tm, 1e-9) / 1e9:6.2f} TF/s")
+if detail == "qr":
+    allc = collections.defaultdict(lambda: [0.0, 0, 0])
+    for i, (kind, probs, ex) in enumerate(ops):
+        if kind != "qr" or not probs:
+            continue
+        mm = max(_dv(p[6], rk) for p in probs); kk = max(_dv(p[7], rk) for p in probs)
+        key = (ex.get("role"), ex.get("cluster"), len(probs), "m%d" % (1 << max(0, mm - 1).bit_length()), "k%d" % (1 << max(0, kk - 1).bit_length()))
+        allc[key][0] += times[i]; allc[key][1] += 1
+    print("all qr ops by (role, cluster, nprob, m, k) pow2 classes:")
+    for k, (tm, c, _) in sorted(allc.items(), key=lambda x: -x[1][0])[:30]:
+        print(f"    {str(k):56s} {c:4d} ops {tm:8.2f} ms  avg {1000 * tm / c:7.1f} us")
