@@ -188,7 +188,8 @@ int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob, const hq_g
    ksplit ignored; mode 2: 64 output rows per CTA (max_rows bounds m), each
    term read coalesced in its own layout (rows across lanes for op(A) = A,
    k across lanes for op(A) = A^T), K split into at most ksplit slices of
-   >= 512 (C zeroed by the caller when ksplit > 1) */
+   >= 512 (C zeroed by the caller when ksplit > 1); modes 3 / 4: mode 2
+   specialised to launches whose terms are all op(A) = A / all op(A) = A^T */
 int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
                    int* rank, int ksplit, int ncmax, int mode, int max_rows, const int* skip);
 int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_piece* pieces,

@@ -337,8 +337,11 @@ __global__ void __launch_bounds__(NT) gemm_rows_kernel(const hq_gemm_prob* __res
 // B (k x NC) is tiny and read through the cache.  K-split slices add into C
 // atomically (the caller zeroed C).
 constexpr int GV_ROWS = 64, GV_U = 8, GV_RQ = GV_ROWS / (NT / 32);
-template <int NC>
-__global__ void __launch_bounds__(NT, 2) gemv_kernel(const hq_gemm_prob* __restrict__ probs,
+// KIND 0: terms of both layouts; 1: only op(A) = A; 2: only op(A) = A^T
+// (the planner knows each launch's layouts; the lean variants keep fewer
+// registers live and run more warps per SM)
+template <int NC, int KIND>
+__global__ void __launch_bounds__(NT, KIND == 1 ? 3 : 2) gemv_kernel(const hq_gemm_prob* __restrict__ probs,
                                                   const hq_gemm_term* __restrict__ terms,
                                                   const int* __restrict__ rank, int ksplit,
                                                   const int* __restrict__ skip) {
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(NT, 2) gemv_kernel(const hq_gemm_prob* __restr
       const int jj = j < n ? j : 0;
       return hq_mask(T.b[(size_t)k * sbk + bj[j]], T.tb == 0 ? k : jj, T.tb == 0 ? jj : k, T.mask_b);
     };
-    if (T.ta == 0) {
+    if (KIND != 2 && (KIND == 1 || T.ta == 0)) {
       if (r < nr) {
         const int gi = i0 + r;
         const double* ap = T.a + gi;
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(NT, 2) gemv_kernel(const hq_gemm_prob* __restr
 #pragma unroll
         for (int j = 0; j < NC; ++j) acc[j] = fma(T.alpha, tacc[j], acc[j]);
       }
-    } else {
+    } else if (KIND != 1) {
       // warp w owns rows rr = w / wpr + (8 / wpr) q of this block and the
       // k-lane-group w % wpr: all its rows advance together, so every k
       // step issues one load per row (independent) plus the B loads
@@ -498,10 +501,16 @@ extern "C" int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob
   if (nprob <= 0) return 0;
   if (ksplit < 1) ksplit = 1;
   cudaStream_t st = (cudaStream_t)stream;
-  if (mode == 2) {
+  if (mode >= 2 && mode <= 4) {
     dim3 grid((max_rows + GV_ROWS - 1) / GV_ROWS, nprob, ksplit);
-    if (ncmax <= 2) gemv_kernel<2><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
-    else gemv_kernel<4><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+    const int kind = mode - 2;
+    if (ncmax <= 2) {
+      if (kind == 1) gemv_kernel<2, 1><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+      else if (kind == 2) gemv_kernel<2, 2><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+      else gemv_kernel<2, 0><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+    } else {
+      gemv_kernel<4, 0><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+    }
     return hq_err(cudaGetLastError());
   }
   if (mode == 1) {

@@ -492,8 +492,11 @@ __device__ void factor_panel_core(const hq_qr_prob& Q, double* P, int ldp, int r
   if (t < NB * NB) S.tp[t] = 0.0;
   __syncthreads();
   HQ_T0
+  // rows per lane E sized to the panel (lanes past the end only cost issue slots)
   if (rows <= 128) panel_factor_reg<4>(P, ldp, rows, pw, Q.tau + p0, S);
+  else if (rows <= 192) panel_factor_reg<6>(P, ldp, rows, pw, Q.tau + p0, S);
   else if (rows <= 256) panel_factor_reg<8>(P, ldp, rows, pw, Q.tau + p0, S);
+  else if (rows <= 384) panel_factor_reg<12>(P, ldp, rows, pw, Q.tau + p0, S);
   else if (rows <= 512) panel_factor_reg<16>(P, ldp, rows, pw, Q.tau + p0, S);
   else if (rows <= 1024) panel_factor_reg<32>(P, ldp, rows, pw, Q.tau + p0, S);
   else panel_factor_block(P, ldp, rows, pw, Q.tau + p0, S);

@@ -452,8 +452,14 @@ class HQREngine(PlanIO):
         """pack (worker threads) -> H2D per matrix as its range is packed ->
         graph replay -> rank table D2H -> per-matrix D2H of the compact factors,
         each matrix assembled on a worker thread as soon as its copy lands."""
+        self.submit(mats)
+        return self.collect()
+
+    def submit(self, mats):
+        """First half of factorize(): pack, upload and launch; returns as soon
+        as the replay is enqueued (the device works while the host goes on)."""
         torch = self.torch
-        tr = [("start", _now())]
+        self._tr = [("start", _now())]
         futs = self.pack_async(mats)
         p = self.plan
         with torch.cuda.stream(self.stream):
@@ -466,12 +472,17 @@ class HQREngine(PlanIO):
                 lo, hi = self.in_ranges[b]
                 if hi > lo:
                     self.d_in[lo:hi].copy_(self.h_in[lo:hi], non_blocking=True)
-        tr.append(("packed", _now()))
+        self._tr.append(("packed", _now()))
         self.execute()
-        tr.append(("replay_enqueued", _now()))
         with torch.cuda.stream(self.stream):
             self.h_tot.copy_(p.totals, non_blocking=True)
             self.h_rk_out.copy_(p.rank, non_blocking=True)
+        self._tr.append(("replay_enqueued", _now()))
+
+    def collect(self):
+        """Second half of factorize(): wait for the run, then D2H + assembly."""
+        torch = self.torch
+        tr = self._tr
         self.stream.synchronize()
         tr.append(("device_done", _now()))
         rk = self.h_rk_out.numpy().copy()
@@ -481,7 +492,6 @@ class HQREngine(PlanIO):
         offs = self.out_offsets(rk)
         self.n_out = int(offs[0][-1])
         self._retune(rk)
-        tr.append(("offsets", _now()))
         pool = _pool()
         jobs = []
         with torch.cuda.stream(self.stream):
@@ -492,10 +502,8 @@ class HQREngine(PlanIO):
                 lo, hi = self.out_range(b, offs)
                 hb = self._pinned_block(hi - lo, taken)
                 taken.append(hb)
-                tr.append((f"pinned{b}", _now()))
                 if hi > lo:
                     hb[:hi - lo].copy_(self.d_out[lo:hi], non_blocking=True)
-                tr.append((f"d2h{b}", _now()))
                 ev = torch.cuda.Event()
                 ev.record(self.stream)
                 jobs.append(pool.submit(self._assemble, b, ev, rk, offs, hb, lo))
@@ -531,6 +539,35 @@ class HQREngine(PlanIO):
     def _assemble(self, b, ev, rk, offs, hb, lo):
         ev.synchronize()
         return PlanIO.factors(self, b, hb.numpy(), rk, offs, False, lo)
+
+
+class HQRPipeline:
+    """A large batch as `parts` engines on their own streams: while one part
+    computes, the next one's inputs go up and the previous one's factors come
+    down (the PCIe traffic of a batch overlaps the device work)."""
+
+    def __init__(self, tree: PartitionTree, batch: int, eps: float = 1e-10, absolute: bool = False,
+                 kcap: int = 512, parts: int = 2, device=None, use_graph: bool = True):
+        if batch < parts:
+            raise ValueError("batch smaller than the number of pipeline parts")
+        sizes = [batch // parts + (1 if i < batch % parts else 0) for i in range(parts)]
+        self.B, self.sizes = batch, sizes
+        self.engines = [HQREngine(tree, sz, eps, absolute, kcap, device=device, use_graph=use_graph)
+                        for sz in sizes]
+
+    def factorize(self, mats):
+        if len(mats) != self.B:
+            raise ValueError(f"expected {self.B} matrices, got {len(mats)}")
+        chunks, o = [], 0
+        for sz in self.sizes:
+            chunks.append(mats[o:o + sz])
+            o += sz
+        for eng, ch in zip(self.engines, chunks):
+            eng.submit(ch)
+        out = []
+        for eng in self.engines:
+            out += eng.collect()
+        return out
 
 
 _ENGINES: dict = {}

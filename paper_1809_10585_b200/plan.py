@@ -304,8 +304,10 @@ class Builder:
         # threads along K for long K, one thread per output row otherwise
         skinny = ncmax <= SKINNY_MAX_COLS
         # skinny products stream their operands (mode 2: coalesced per term
-        # layout, per-problem K slices); modes 0/1 remain in the ABI
-        mode = 2
+        # layout, per-problem K slices; 3 / 4 when every term is A / A^T);
+        # modes 0/1 remain in the ABI
+        tas = {t[2] for p in probs for t in p[5]}
+        mode = 3 if tas == {0} else (4 if tas == {1} else 2)
         if skinny and mode == 0 and ksplit > 1:
             # a K-slice of >= 8 k per thread amortizes the CTA reduction
             # (only ever lowered: the caller zeroed C for ksplit > 1)

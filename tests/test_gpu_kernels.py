@@ -96,7 +96,7 @@ def test_gemm_terms_masks(dev, m, n, k, ta, tb, ks, masks, tile):
     assert np.allclose(back(dC, m, n), ref, atol=1e-11 * max(1, np.abs(ref).max()))
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("m,n,k,ta,tb,ks,masks", [(16, 2, 8192, 1, 0, 32, (0, 0)), (2, 2, 5000, 1, 0, 19, (0, 0)),
                                                   (256, 2, 256, 0, 0, 1, (1, 0)), (37, 3, 300, 1, 1, 1, (2, 0)),
                                                   (70, 4, 900, 0, 1, 4, (0, 0)), (5, 1, 3, 1, 0, 1, (0, 0)),
@@ -108,16 +108,19 @@ def test_gemm_skinny(dev, m, n, k, ta, tb, ks, masks, mode):
     rng = np.random.default_rng(m * 7 + n + k)
     A = rng.standard_normal((k, m) if ta else (m, k))
     B = rng.standard_normal((n, k) if tb else (k, n))
+    if (mode == 3 and ta) or (mode == 4 and not ta):
+        pytest.skip("layout-specialised mode: every term must match it")
+    ta2 = 1 if mode == 4 else 0   # second term's layout (mode 4: all op(A) = A^T)
     A2 = rng.standard_normal((m, 5))
     B2 = rng.standard_normal((5, n))
     if mode == 1:
         ks = 1
     C = rng.standard_normal((m, n)) if ks == 1 else np.zeros((m, n))
-    dA, dB, dA2, dB2, dC = (colmajor(torch, x) for x in (A, B, A2, B2, C))
+    dA, dB, dA2, dB2, dC = (colmajor(torch, x) for x in (A, B, A2.T if ta2 else A2, B2, C))
     rank = torch.zeros(4, dtype=torch.int32, device="cuda")
     terms = np.zeros(2, _abi.GEMM_TERM)
     terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, masks[0], masks[1], 0.75)
-    terms[1] = (dA2.data_ptr(), dB2.data_ptr(), m, 5, 0, 0, 5, -1, 0, 0, -1.0)
+    terms[1] = (dA2.data_ptr(), dB2.data_ptr(), 5 if ta2 else m, 5, ta2, 0, 5, -1, 0, 0, -1.0)
     probs = np.zeros(1, _abi.GEMM_PROB)
     beta = 0.5 if ks == 1 else 0.0
     probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta)
