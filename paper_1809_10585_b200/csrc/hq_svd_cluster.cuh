@@ -139,9 +139,9 @@ __device__ __noinline__ void svd_cluster_body(const hq_svd_prob& P, int* __restr
           double a = act ? nrmb[p] : 0.0, b = act ? nrmb[q] : 0.0;
           double* Bb = bk ? B1 : B0;
           double xp[E];
-          const bool rr = jacobi_pair<LP, E, false>(xp, Bb + (size_t)p * ld, Bb + (size_t)q * ld, a, b, ld, tol2,
-                                                    tiny2, thr2, gl, act, S.trash);
-          if (rr && gl == 0) { nrmb[p] = a; nrmb[q] = b; S.rot = 1; }
+          const int rr = jacobi_pair<LP, E, false>(xp, Bb + (size_t)p * ld, Bb + (size_t)q * ld, a, b, ld, tol2,
+                                                   tiny2, thr2, gl, act, S.trash);
+          if (rr && gl == 0) { nrmb[p] = a; nrmb[q] = b; if (rr > 1) S.rot = 1; }
         }
         __syncthreads();
       }
@@ -171,10 +171,10 @@ __device__ __noinline__ void svd_cluster_body(const hq_svd_prob& P, int* __restr
             if (!own) j = 0;
             const bool act = own && col1[j] >= 0;
             double b = act ? nrm1[j] : 0.0;
-            const bool rr = jacobi_pair<LP, E, true>(xp, B0, B1 + (size_t)j * ld, a, b, ld, tol2, tiny2, thr2, gl,
+            const int rr = jacobi_pair<LP, E, true>(xp, B0, B1 + (size_t)j * ld, a, b, ld, tol2, tiny2, thr2, gl,
                                                      act, S.trash);
             if (rr && gl == 0) nrm1[j] = b;
-            any |= rr;
+            any |= rr > 1;
           }
 #ifdef HQ_DEBUG_SWEEPS
           const long long q1 = clock64();
@@ -202,10 +202,10 @@ __device__ __noinline__ void svd_cluster_body(const hq_svd_prob& P, int* __restr
             bool act = i < bs && col0[i] >= 0 && col1[j] >= 0;
             double a = act ? nrm0[i] : 0.0, b = act ? nrm1[j] : 0.0;
             double xp[E];
-            const bool rr = jacobi_pair<LP, E, false>(xp, B0 + (size_t)(act ? i : 0) * ld,
+            const int rr = jacobi_pair<LP, E, false>(xp, B0 + (size_t)(act ? i : 0) * ld,
                                                       B1 + (size_t)(act ? j : 0) * ld, a, b, ld, tol2, tiny2, thr2,
                                                       gl, act, S.trash);
-            if (rr && gl == 0) { nrm0[i] = a; nrm1[j] = b; S.rot = 1; }
+            if (rr && gl == 0) { nrm0[i] = a; nrm1[j] = b; if (rr > 1) S.rot = 1; }
           }
           __syncthreads();
         }
