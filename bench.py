@@ -4,7 +4,7 @@
 Workload (BASELINE.json metric "at n=16384"): config 2, the ill-conditioned
 HODLR matrix, n = 16384, leaf 256, off-diagonal rank 16, A = D B with
 D = diag(logspace(0,-14,n)) permuted, tol 1e-10 relative.  One step = one
-batch of B independent such matrices (seeds B*rank .. B*rank+B-1; B = 48, or fewer
+batch of B independent such matrices (seeds B*rank .. B*rank+B-1; B = 64, or fewer
 if they do not fit 85 % of the free HBM) factorized
 by one graph replay: power iteration for ||A||_2, the unrolled Algorithm 2,
 compaction of Y, T, R.  `latency_ms_single_matrix` reports one matrix alone.
@@ -55,7 +55,7 @@ def parse():
                    help="rank capacity of the plan (overflow raises RankCapacityError, never truncates)")
     p.add_argument("--no-instrument", action="store_true")
     p.add_argument("--batch", type=int, default=None,
-                   help="matrices per step per GPU (config 2 default: 48 or what fits; config 4 is the fixed 64-batch)")
+                   help="matrices per step per GPU (config 2 default: 64 or what fits; config 4 is the fixed 64-batch)")
     return p.parse_args()
 
 
@@ -218,7 +218,7 @@ def instrument(eng, torch):
     return per
 
 
-def auto_batch(torch, ci, n, tol, local, cap=48, kcap=256):
+def auto_batch(torch, ci, n, tol, local, cap=64, kcap=192):
     """Matrices per step: as many as fit 85 % of the free HBM (the arena of a
     one-matrix plan scales linearly with the batch), at most `cap`."""
     from paper_1809_10585_b200.gen import gen_config
@@ -252,20 +252,34 @@ def main():
         seeds = shard_seeds(total_batch, ws, rank)
         scaling = "strong"
     else:
-        per = args.batch or auto_batch(torch, args.config, n, cfg["tol"], local)
+        per = args.batch or auto_batch(torch, args.config, n, cfg["tol"], local, kcap=args.kcap or 192)
         seeds = list(range(rank * per, (rank + 1) * per))
         scaling = "weak"
     mats = [gen_config(args.config, seed=s, n=n) for s in seeds]
     a = mats[0]
-    # rank capacity 256 (max rank seen on this workload: 158); an overflow
-    # raises RankCapacityError, it never truncates
-    kcap = args.kcap or (256 if total_batch == 1 else 512)
-    eng = HQREngine(a.tree(), len(mats), cfg["tol"], kcap=kcap, device=f"cuda:{local}")
-    eng.pack(mats)
-    eng.upload()
-    eng.snapshot_device_input()
-    eng.execute()  # capture + first run
-    eng.download()
+    # rank capacity 192 (largest rank on this workload over 64 seeds: 159); an
+    # overflow raises RankCapacityError -- it never truncates -- and the run
+    # is redone at capacity 512 with the batch that fits
+    from paper_1809_10585_b200.hqr import RankCapacityError
+    kcap = args.kcap or (192 if total_batch == 1 else 512)
+    while True:
+        eng = HQREngine(a.tree(), len(mats), cfg["tol"], kcap=kcap, device=f"cuda:{local}")
+        eng.pack(mats)
+        eng.upload()
+        eng.snapshot_device_input()
+        eng.execute()  # capture + first run
+        try:
+            eng.download()
+            break
+        except RankCapacityError:
+            if kcap >= 512:
+                raise
+            del eng
+            torch.cuda.empty_cache()
+            kcap = 512
+            if total_batch == 1 and not args.batch:
+                mats = mats[:auto_batch(torch, args.config, n, cfg["tol"], local, kcap=kcap)]
+                a = mats[0]
     s = eng.stream
 
     def barrier():
