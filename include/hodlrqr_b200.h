@@ -77,8 +77,10 @@ typedef struct hq_concat_prob {
 } hq_concat_prob;
 
 /* in-place Householder QR of W (m x k): R on/above the diagonal, unit-lower
-   reflectors below, gamma in tau, per-panel T in tpanel; optional full
-   compact-WY T (k x k) into tfull (reference: wy.py:17-72, dense.py:45-68) */
+   reflectors below, gamma in tau, per-panel T in tpanel (ceil(r/16) blocks of
+   16 x 16, r = min(m, k)); optional full compact-WY T (r x r) into tfull
+   (reference: wy.py:17-72, dense.py:45-68).  With tfull and cluster >= 2,
+   tpanel must have room for 2 * r * 16 more doubles (merge scratch). */
 typedef struct hq_qr_prob {
   double* w;
   double* tau;

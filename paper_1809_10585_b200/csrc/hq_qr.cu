@@ -484,6 +484,87 @@ __device__ __noinline__ void merge_T(const hq_qr_prob& Q, const double* W, int l
   }
 }
 
+// Cluster mode splits the full-T merge of panel p over the CTAs that are not
+// factoring, pipelined one phase apart so it never extends a phase:
+//   phase p+1: X_p = Y[:,0:p0]^T Y_p (p0 x pw, DMMA tiles split over the
+//              parts) into a global scratch (double-buffered by panel parity);
+//              part 0 also stores T_p's diagonal block into tfull;
+//   phase p+2: T[0:p0, p0:p0+pw] = -T11 (X_p T_p) (tiles split over the
+//              parts; T11 complete since panel p-1's merge ran in phase p+1).
+// Visibility between phases comes from the cluster barrier ending a phase.
+__device__ __noinline__ void merge_X_split(const hq_qr_prob& Q, const double* W, int ld, int m, int r, int p0,
+                                           double* X, int part, int nparts, QrSmem& S) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int pw = min(NB, r - p0), rows = m - p0;
+  const int gq = lane >> 2, tq = lane & 3;
+  if (part == 0) {
+    const double* tp_ = Q.tpanel + (size_t)(p0 / NB) * NB * NB;
+    for (int e = t; e < pw * pw; e += NT)
+      Q.tfull[(p0 + e % pw) + (size_t)(p0 + e / pw) * Q.ldt] = tp_[e % pw + (e / pw) * NB];
+  }
+  if (p0 == 0) return;
+  const double* P = W + p0 + (size_t)p0 * ld;
+  const int ntm = (p0 + 7) / 8;
+  for (int tile = part * NW + wid; tile < ntm * 2; tile += nparts * NW) {
+    const int mt = tile >> 1, nt = tile & 1;
+    const int b = mt * 8 + gq, a = nt * 8 + gq;
+    double d0 = 0.0, d1 = 0.0;
+    dmma_kloop(d0, d1, 0, rows, [&](int k0, double (&av)[8], double (&bv)[8]) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = k0 + 4 * u + tq;
+        av[u] = (i < rows && b < p0) ? W[(p0 + i) + (size_t)b * ld] : 0.0;
+        bv[u] = (i < rows && a < pw) ? yval(P, ld, i, a) : 0.0;
+      }
+    });
+    const int ro = mt * 8 + gq, c = nt * 8 + 2 * tq;
+    if (ro < p0) { X[ro + (size_t)c * r] = d0; X[ro + (size_t)(c + 1) * r] = d1; }
+  }
+}
+
+__device__ __noinline__ void merge_T12_split(const hq_qr_prob& Q, int r, int p0, const double* X, int part,
+                                             int nparts, QrSmem& S) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int pw = min(NB, r - p0);
+  if (p0 == 0) return;
+  const int gq = lane >> 2, tq = lane & 3;
+  const double* tp_ = Q.tpanel + (size_t)(p0 / NB) * NB * NB;
+  double* TF = Q.tfull;
+  const int ldt = Q.ldt;
+  // X' = X T_p for every row (cheap, redundant per part) into shared memory
+  for (int b = t; b < p0; b += NT) {
+    double xr[NB];
+#pragma unroll
+    for (int a = 0; a < NB; ++a) xr[a] = a < pw ? X[b + (size_t)a * r] : 0.0;
+#pragma unroll
+    for (int a = 0; a < NB; ++a) {
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        if (c <= a) v = fma(xr[c], tp_[c + a * NB], v);
+      S.ybuf[b + a * XS_LD] = a < pw ? v : 0.0;
+    }
+  }
+  __syncthreads();
+  const int ntm = (p0 + 7) / 8;
+  for (int tile = part * NW + wid; tile < ntm * 2; tile += nparts * NW) {
+    const int mt = tile >> 1, nt = tile & 1;
+    const int rr = mt * 8 + gq, a = nt * 8 + gq;
+    double d0 = 0.0, d1 = 0.0;
+    dmma_kloop(d0, d1, mt * 8, p0, [&](int k0, double (&av)[8], double (&bv)[8]) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = k0 + 4 * u + tq;
+        av[u] = (rr < p0 && c < p0 && c >= rr) ? -TF[rr + (size_t)c * ldt] : 0.0;
+        bv[u] = (c < p0 && a < pw) ? S.ybuf[c + a * XS_LD] : 0.0;
+      }
+    });
+    const int ro = mt * 8 + gq, co = nt * 8 + 2 * tq;
+    if (ro < p0 && co < pw) TF[ro + (size_t)(p0 + co) * ldt] = d0;
+    if (ro < p0 && co + 1 < pw) TF[ro + (size_t)(p0 + co + 1) * ldt] = d1;
+  }
+}
+
 // Reduce panel p0 held at P (rows x pw, ld ldp; shared or global) into R +
 // unit lower reflectors; publish gamma (tau) and T_p (S.tp, Q.tpanel).
 __device__ void factor_panel_core(const hq_qr_prob& Q, double* P, int ldp, int rows, int pw, int p0,
@@ -567,11 +648,14 @@ __global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __r
 #ifdef HQ_DEBUG_TIMING
   long long tph = clock64();
 #endif
-  for (int ph = 0; ph <= np; ++ph) {
+  // with a full T, one extra phase finishes the pipelined merge of the last panel
+  const int nph = np + (Q.tfull && np > 0 ? 1 : 0);
+  double* Xs = Q.tpanel + (size_t)np * NB * NB;   // merge scratch: 2 x (r x NB)
+  for (int ph = 0; ph <= nph; ++ph) {
 #ifdef HQ_DEBUG_TIMING
     long long tA = clock64(), tB = tA, tC = tA;
 #endif
-    if (ph >= 1) {
+    if (ph >= 1 && ph <= np) {
       const int q0 = (ph - 1) * NB, qw = min(NB, r - q0), rows = m - q0;
       if (t < NB * NB) S.tp[t] = Q.tpanel[(size_t)(ph - 1) * NB * NB + t];
       const double* Yg = W + q0 + (size_t)q0 * ld;
@@ -635,14 +719,25 @@ __global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __r
           }
         }
       }
-      // the full compact-WY T block of panel ph-1 is merged one phase later
-      // by a CTA that is not factoring (off the panel chain)
-      if (Q.tfull && cr == (ph + 1) % G) {
-        __syncthreads();
-        merge_T(Q, W, ld, m, r, q0, Yg, ld, S.tp, S);
-      }
-    } else if (np > 0 && cr == 0) {
+    } else if (ph == 0 && np > 0 && cr == 0) {
       factor_panel_step(Q, W, ld, m, k, r, 0, false, false, S);
+    }
+    // full compact-WY T: the CTAs not factoring this phase form X of panel
+    // ph-1 and the T12 block of panel ph-2 (split merge, see merge_X_split)
+    if (Q.tfull && ph >= 1) {
+      const bool fact_now = ph < np;
+      const int fct = ph % G;
+      if (!(fact_now && cr == fct)) {
+        const int nparts = fact_now ? G - 1 : G;
+        const int part = fact_now ? (cr - fct - 1 + G) % G : cr;
+        __syncthreads();
+        if (ph - 1 < np) merge_X_split(Q, W, ld, m, r, (ph - 1) * NB, Xs + (size_t)((ph - 1) & 1) * r * NB,
+                                       part, nparts, S);
+        if (ph >= 2) {
+          __syncthreads();
+          merge_T12_split(Q, r, (ph - 2) * NB, Xs + (size_t)((ph - 2) & 1) * r * NB, part, nparts, S);
+        }
+      }
     }
     __syncthreads();
 #ifdef HQ_DEBUG_TIMING

@@ -541,35 +541,6 @@ class HQREngine(PlanIO):
         return PlanIO.factors(self, b, hb.numpy(), rk, offs, False, lo)
 
 
-class HQRPipeline:
-    """A large batch as `parts` engines on their own streams: while one part
-    computes, the next one's inputs go up and the previous one's factors come
-    down (the PCIe traffic of a batch overlaps the device work)."""
-
-    def __init__(self, tree: PartitionTree, batch: int, eps: float = 1e-10, absolute: bool = False,
-                 kcap: int = 512, parts: int = 2, device=None, use_graph: bool = True):
-        if batch < parts:
-            raise ValueError("batch smaller than the number of pipeline parts")
-        sizes = [batch // parts + (1 if i < batch % parts else 0) for i in range(parts)]
-        self.B, self.sizes = batch, sizes
-        self.engines = [HQREngine(tree, sz, eps, absolute, kcap, device=device, use_graph=use_graph)
-                        for sz in sizes]
-
-    def factorize(self, mats):
-        if len(mats) != self.B:
-            raise ValueError(f"expected {self.B} matrices, got {len(mats)}")
-        chunks, o = [], 0
-        for sz in self.sizes:
-            chunks.append(mats[o:o + sz])
-            o += sz
-        for eng, ch in zip(self.engines, chunks):
-            eng.submit(ch)
-        out = []
-        for eng in self.engines:
-            out += eng.collect()
-        return out
-
-
 _ENGINES: dict = {}
 
 

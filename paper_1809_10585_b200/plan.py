@@ -598,7 +598,8 @@ class Builder:
             mcap = nl + sum(s[4] for s in sl)
             panel = self._ph(mcap * nl)
             tau = self._ph(nl)
-            tp = self._ph(math.ceil(nl / NB) * NB * NB)
+            # panel T's + the cluster kernel's full-T merge scratch (2 x nl x NB)
+            tp = self._ph(math.ceil(nl / NB) * NB * NB + 2 * nl * NB)
             m_ri = self.slots.take()
             gat.append((d["leafA"][v], panel, nl, mcap, [(s[0], s[1], s[2], s[2], s[3]) for s in sl],
                         m_ri))

@@ -153,7 +153,7 @@ def test_qr_and_applyq(dev, m, k, cl):
     dW = colmajor(torch, A)
     r = min(m, k)
     tau = torch.zeros(max(r, 1), dtype=torch.float64, device="cuda")
-    tp = torch.zeros(((r + 15) // 16) * 256 + 256, dtype=torch.float64, device="cuda")
+    tp = torch.zeros(((r + 15) // 16) * 256 + 2 * r * 16 + 256, dtype=torch.float64, device="cuda")
     tf = torch.full((r * r + 32 * r,), float("nan"), dtype=torch.float64, device="cuda")
     rank = torch.zeros(4, dtype=torch.int32, device="cuda")
     q = np.zeros(1, _abi.QR_PROB)

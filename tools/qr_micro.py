@@ -12,7 +12,7 @@ for m, k, full, cl in [(352, 256, 1, 1), (352, 256, 1, 8), (352, 256, 0, 8), (25
         dW = torch.tensor(A.T.copy(), device="cuda")
         r = min(m, k)
         tau = torch.zeros(r, dtype=torch.float64, device="cuda")
-        tp = torch.zeros(((r + 15) // 16) * 256, dtype=torch.float64, device="cuda")
+        tp = torch.zeros(((r + 15) // 16) * 256 + 2 * r * 16, dtype=torch.float64, device="cuda")
         tf = torch.zeros(r * r, dtype=torch.float64, device="cuda")
         rank = torch.zeros(4, dtype=torch.int32, device="cuda")
         q = np.zeros(1, _abi.QR_PROB)

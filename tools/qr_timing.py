@@ -15,7 +15,7 @@ full = 1
 A = np.random.default_rng(1).standard_normal((m, k))
 for rep in range(2):
     dW = torch.tensor(A.T.copy(), device="cuda"); r = min(m, k)
-    tau = torch.zeros(r, dtype=torch.float64, device="cuda"); tp = torch.zeros(((r + 15) // 16) * 256, dtype=torch.float64, device="cuda")
+    tau = torch.zeros(r, dtype=torch.float64, device="cuda"); tp = torch.zeros(((r + 15) // 16) * 256 + 2 * r * 16, dtype=torch.float64, device="cuda")
     tf = torch.zeros(r * r, dtype=torch.float64, device="cuda"); rank = torch.zeros(4, dtype=torch.int32, device="cuda")
     q = np.zeros(1, _abi.QR_PROB); q[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), tf.data_ptr() if full else 0, m, r, m, -1, k, -1)
     dq = put(q); torch.cuda.synchronize()
