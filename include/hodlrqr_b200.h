@@ -51,7 +51,7 @@ typedef struct hq_gemm_prob {
   int32_t ldc;
   int32_t m, m_ri, n, n_ri;
   int32_t term0, nterm;
-  int32_t pad_;
+  int32_t item0;   /* hq_gemm_skinny mode 5: first work item of this problem */
   double beta;
 } hq_gemm_prob;
 
@@ -191,7 +191,11 @@ int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob, const hq_g
    term read coalesced in its own layout (rows across lanes for op(A) = A,
    k across lanes for op(A) = A^T), K split into at most ksplit slices of
    >= 512 (C zeroed by the caller when ksplit > 1); modes 3 / 4: mode 2
-   specialised to launches whose terms are all op(A) = A / all op(A) = A^T */
+   specialised to launches whose terms are all op(A) = A / all op(A) = A^T;
+   mode 5: one launch over problems of different K (all op(A) = A^T, one term
+   each): problem i owns work items [item0_i, item0_{i+1}) -- its K slices --
+   and the grid is ksplit = the total item count; every CTA covers all
+   output rows of its problem (C zeroed by the caller) */
 int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
                    int* rank, int ksplit, int ncmax, int mode, int max_rows, const int* skip);
 int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_piece* pieces,

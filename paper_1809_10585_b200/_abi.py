@@ -22,7 +22,7 @@ GEMM_TERM = np.dtype([("a", P), ("b", P), ("lda", I), ("ldb", I), ("ta", I), ("t
                       ("k", I), ("k_ri", I), ("mask_a", I), ("mask_b", I),
                       ("alpha", np.float64)], align=True)
 GEMM_PROB = np.dtype([("c", P), ("ldc", I), ("m", I), ("m_ri", I), ("n", I), ("n_ri", I),
-                      ("term0", I), ("nterm", I), ("pad_", I), ("beta", np.float64)], align=True)
+                      ("term0", I), ("nterm", I), ("item0", I), ("beta", np.float64)], align=True)
 PIECE = np.dtype([("p", P), ("ld", I), ("cols", I), ("cols_ri", I), ("pad_", I),
                   ("alpha", np.float64)], align=True)
 CONCAT_PROB = np.dtype([("dst", P), ("dst2", P), ("ldd", I), ("ldd2", I), ("rows", I),

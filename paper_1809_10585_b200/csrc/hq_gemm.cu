@@ -490,6 +490,97 @@ __global__ void __launch_bounds__(NT, KIND == 1 ? 3 : 2) gemv_kernel(const hq_ge
     else *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
   }
 }
+// Mode 5: the power iteration's V^T X products of every tree level in ONE
+// launch.  Problem i owns the work items [item0_i, item0_{i+1}) (its K
+// slices, sized on the host from the static block sizes), so the grid has no
+// empty CTAs; a CTA finds its problem by binary search, then covers all output
+// rows of that problem for its K slice: warp w takes rows w, w+8, ... (RQ at a
+// time, one independent load per row per k step), lanes along k, shuffle
+// reduction, atomic add into C (zeroed by the caller).
+template <int NC>
+__global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __restrict__ probs,
+                                                       const hq_gemm_term* __restrict__ terms,
+                                                       const int* __restrict__ rank, int nprob, int nitems,
+                                                       const int* __restrict__ skip) {
+  if (skip && *skip) return;
+  constexpr int RQ = 4;
+  const int bid = blockIdx.x;
+  int lo = 0, hi = nprob - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (probs[mid].item0 <= bid) lo = mid; else hi = mid - 1;
+  }
+  const hq_gemm_prob P = probs[lo];
+  const int ks = (lo + 1 < nprob ? probs[lo + 1].item0 : nitems) - P.item0;
+  const int z = bid - P.item0;
+  const int m = hq_dim(rank, P.m, P.m_ri), n = hq_dim(rank, P.n, P.n_ri);
+  if (m <= 0 || n <= 0 || z < 0 || z >= ks) return;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  for (int ti = 0; ti < P.nterm; ++ti) {
+    const hq_gemm_term T = terms[P.term0 + ti];
+    const int kd = hq_dim(rank, T.k, T.k_ri);
+    const int kb = (int)(((long long)kd * z) / ks), ke = (int)(((long long)kd * (z + 1)) / ks);
+    if (kb >= ke) continue;
+    const size_t sbk = T.tb == 0 ? 1 : (size_t)T.ldb, sbj = T.tb == 0 ? (size_t)T.ldb : 1;
+    if (T.ta == 0) {
+      // rows across threads (coalesced columns of A)
+      for (int i = t; i < m; i += NT) {
+        double d[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) d[j] = 0.0;
+        for (int k = kb; k < ke; ++k) {
+          const double a = hq_mask(T.a[i + (size_t)k * T.lda], i, k, T.mask_a);
+#pragma unroll
+          for (int j = 0; j < NC; ++j) {
+            const int jj = j < n ? j : 0;
+            d[j] = fma(a, hq_mask(T.b[(size_t)k * sbk + jj * sbj], T.tb == 0 ? k : jj, T.tb == 0 ? jj : k,
+                                  T.mask_b), d[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+          if (j < n) atomicAdd(P.c + i + (size_t)j * P.ldc, T.alpha * d[j]);
+      }
+      continue;
+    }
+    const bool plain = T.mask_a == 0 && T.mask_b == 0;
+    for (int r0 = wid; r0 < m; r0 += (NT / 32) * RQ) {
+      double d[RQ][NC];
+#pragma unroll
+      for (int q = 0; q < RQ; ++q)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) d[q][j] = 0.0;
+      const double* ap0 = T.a + (size_t)r0 * T.lda;
+      const size_t rstep = (size_t)(NT / 32) * T.lda;
+      const int nq = min(RQ, (m - 1 - r0) / (NT / 32) + 1);
+      for (int k = kb + lane; k < ke; k += 32) {
+        double b[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const int jj = j < n ? j : 0;
+          const double v = __ldg(T.b + (size_t)k * sbk + jj * sbj);
+          b[j] = plain ? v : hq_mask(v, T.tb == 0 ? k : jj, T.tb == 0 ? jj : k, T.mask_b);
+        }
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+          const double v = __ldg(ap0 + (q < nq ? q * rstep : 0) + k);
+          const double a = plain ? v : hq_mask(v, k, r0 + (NT / 32) * q, T.mask_a);
+#pragma unroll
+          for (int j = 0; j < NC; ++j) d[q][j] = fma(a, b[j], d[q][j]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < RQ; ++q) {
+        if (q >= nq) break;   // warp-uniform
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const double v = warp_sum(d[q][j]);
+          if (lane == 0 && j < n) atomicAdd(P.c + (r0 + (NT / 32) * q) + (size_t)j * P.ldc, T.alpha * v);
+        }
+      }
+    }
+  }
+}
 }  // namespace
 
 // skinny products (n <= 4 output columns).  mode 0: grid (ksplit, nprob),
@@ -501,6 +592,12 @@ extern "C" int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob
   if (nprob <= 0) return 0;
   if (ksplit < 1) ksplit = 1;
   cudaStream_t st = (cudaStream_t)stream;
+  if (mode == 5) {
+    // ksplit carries the total work-item count of the launch
+    if (ncmax <= 2) gemv_flat_kernel<2><<<ksplit, NT, 0, st>>>(probs, terms, rank, nprob, ksplit, skip);
+    else gemv_flat_kernel<4><<<ksplit, NT, 0, st>>>(probs, terms, rank, nprob, ksplit, skip);
+    return hq_err(cudaGetLastError());
+  }
   if (mode >= 2 && mode <= 4) {
     dim3 grid((max_rows + GV_ROWS - 1) / GV_ROWS, nprob, ksplit);
     const int kind = mode - 2;

@@ -365,16 +365,16 @@ class Builder:
                     p1.append((buf, kc, Dim(kc, R[u]), Dim(ncap, nris[b]), 0.0, [term]))
                     zeros.append((buf, kc * ncap))
         if p1 and ncap <= SKINNY_MAX_COLS:
-            # streaming V^T X products: one launch per block size (tree level)
-            # with its own K split, so no launch carries empty slices
-            groups = {}
-            for prob, z in zip(p1, zeros):
-                groups.setdefault(prob[5][0][8].cap, []).append((prob, z))
-            for kk in sorted(groups, reverse=True):
-                ks = max(1, min(32, kk // 512))
-                if ks > 1:
-                    self.zero([z for _, z in groups[kk]])
-                self.gemm([pr for pr, _ in groups[kk]], skip=skip, ksplit=ks)
+            # streaming V^T X products of every level in one launch (mode 5):
+            # each problem gets ceil-ish K/512 work items (<= 32), listed by
+            # prefix sums; outputs are zeroed and accumulated atomically
+            items, tot = [], 0
+            for prob in p1:
+                items.append(tot)
+                tot += max(1, min(32, sum(t[8].cap for t in prob[5]) // 512))
+            self.zero(zeros)
+            self.op("gemm", p1, dict(tiles=1, ksplit=tot, skip=skip, skinny=True, ncmax=ncap, mode=5,
+                                     max_rows=max(pr[2].cap for pr in p1), tile=64, items=items))
         elif p1:
             ksplit = 1
             if kmax >= 1024:
@@ -1080,7 +1080,8 @@ class CompiledPlan:
                 ta = np.zeros(nterm, _abi.GEMM_TERM)
                 ti = 0
                 for i, (c, ldc, m, n, beta, terms) in enumerate(probs):
-                    pa[i] = (A(c), ldc, m.cap, m.ri, n.cap, n.ri, ti, len(terms), 0, beta)
+                    pa[i] = (A(c), ldc, m.cap, m.ri, n.cap, n.ri, ti, len(terms),
+                             extra.get("items", [0] * len(probs))[i], beta)
                     for (a, lda, tra, ma, bb, ldb, trb, mb, k, alpha) in terms:
                         ta[ti] = (A(a), A(bb), lda, ldb, tra, trb, k.cap, k.ri, ma, mb, alpha)
                         ti += 1

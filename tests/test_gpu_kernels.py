@@ -96,7 +96,7 @@ def test_gemm_terms_masks(dev, m, n, k, ta, tb, ks, masks, tile):
     assert np.allclose(back(dC, m, n), ref, atol=1e-11 * max(1, np.abs(ref).max()))
 
 
-@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("m,n,k,ta,tb,ks,masks", [(16, 2, 8192, 1, 0, 32, (0, 0)), (2, 2, 5000, 1, 0, 19, (0, 0)),
                                                   (256, 2, 256, 0, 0, 1, (1, 0)), (37, 3, 300, 1, 1, 1, (2, 0)),
                                                   (70, 4, 900, 0, 1, 4, (0, 0)), (5, 1, 3, 1, 0, 1, (0, 0)),
@@ -115,14 +115,15 @@ def test_gemm_skinny(dev, m, n, k, ta, tb, ks, masks, mode):
     B2 = rng.standard_normal((5, n))
     if mode == 1:
         ks = 1
-    C = rng.standard_normal((m, n)) if ks == 1 else np.zeros((m, n))
+    accumulate = ks > 1 or mode == 5   # mode 5 always adds into a zeroed C
+    C = np.zeros((m, n)) if accumulate else rng.standard_normal((m, n))
     dA, dB, dA2, dB2, dC = (colmajor(torch, x) for x in (A, B, A2.T if ta2 else A2, B2, C))
     rank = torch.zeros(4, dtype=torch.int32, device="cuda")
     terms = np.zeros(2, _abi.GEMM_TERM)
     terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, masks[0], masks[1], 0.75)
     terms[1] = (dA2.data_ptr(), dB2.data_ptr(), 5 if ta2 else m, 5, ta2, 0, 5, -1, 0, 0, -1.0)
     probs = np.zeros(1, _abi.GEMM_PROB)
-    beta = 0.5 if ks == 1 else 0.0
+    beta = 0.0 if accumulate else 0.5
     probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta)
     dt, dp = put(torch, terms), put(torch, probs)
     assert lib.hq_gemm_skinny(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), ks, n, mode, m, None) == 0

@@ -11,7 +11,7 @@ B = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 c = gen.CONFIGS[ci]
 mats = [gen.gen_config(ci, seed=s, n=n) for s in range(B)]
 a = mats[0]
-eng = HQREngine(a.tree(), B, c["tol"], kcap=256 if B > 1 else 512, use_graph=False)
+eng = HQREngine(a.tree(), B, c["tol"], kcap=192 if B > 1 else 512, use_graph=False)
 eng.factorize(mats)
 rk = eng.h_rk_out.numpy()
 plan = eng.plan
