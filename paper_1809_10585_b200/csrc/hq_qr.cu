@@ -27,7 +27,6 @@ namespace {
 constexpr int NT = 256, NW = NT / 32, NB = 16;
 constexpr int STAGE_ROWS = 1024;  // panel staged in smem when rows <= STAGE_ROWS
 constexpr int CW = 32;            // trailing-update column chunk
-constexpr int MAXK_T = 384;       // max columns when the full compact-WY T is formed
 constexpr int YBUF = 528 * NB;    // staged Y / X chunk / merge scratch (doubles)
 constexpr int XS_LD = 388;        // merge scratch leading dim (== 4 mod 16)
 // W = Y^T X is kept transposed (wc[col + refl * WLD]) and T^op W as
