@@ -293,12 +293,23 @@ class HQREngine(PlanIO):
     """PlanIO + device arena + CUDA graph for batched hQR of same-shape matrices."""
 
     def __init__(self, tree: PartitionTree, batch: int = 1, eps: float = 1e-10,
-                 absolute: bool = False, kcap: int = 512, device=None, use_graph: bool = True):
+                 absolute: bool = False, kcap: int = 512, device=None, use_graph: bool = True,
+                 stream_out: bool = False):
+        """stream_out: keep the compact output stream in its own region and
+        run its compaction outside the graph, so factorize_stream() can copy
+        one run's factors to the host while the next run computes (costs the
+        output region's memory, which otherwise aliases scratch)."""
         torch = _require_cuda()
         super().__init__(tree, batch, eps, absolute, kcap)
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
-        self.plan = CompiledPlan(self.builder, self.device)
+        self.stream_out = bool(stream_out)
+        self.plan = CompiledPlan(self.builder, self.device, alias_out=not self.stream_out)
+        last = self.builder.ops[-1]
+        assert last[0] == "pack_copy" and last[2].get("which") == 0, "plan must end with the output compaction"
+        self._tail = len(self.plan.launch) - 1 if self.stream_out else None
+        self._d2h_done = None
+        self._step = 0
         pin = lambda a: torch.from_numpy(a).pin_memory()
         self.h_rk, self.h_sc, self.h_px = pin(self.rk), pin(self.sc), pin(self.px)
         self.rk, self.sc, self.px = self.h_rk.numpy(), self.h_sc.numpy(), self.h_px.numpy()
@@ -307,8 +318,11 @@ class HQREngine(PlanIO):
         in_cap, out_cap = self.inbuf.size, self.outbuf.size
         self.h_in = self.h_out = None
         self.inbuf = self.outbuf = None
-        self.h_rk_out = torch.zeros_like(self.h_rk).pin_memory()
-        self.h_tot = torch.zeros(2, dtype=torch.int64).pin_memory()
+        # rank table / totals read back per run: two pinned copies (a stream of
+        # runs reads one while the next run's copy lands in the other)
+        self._h_rk_outs = [torch.zeros_like(self.h_rk).pin_memory() for _ in range(2)]
+        self._h_tots = [torch.zeros(2, dtype=torch.int64).pin_memory() for _ in range(2)]
+        self.h_rk_out, self.h_tot = self._h_rk_outs[0], self._h_tots[0]
         p = self.plan
         ib, ob = p.bases[R_IN], p.bases[R_OUT]
         self.d_in = p.arena[ib:ib + in_cap]
@@ -319,6 +333,7 @@ class HQREngine(PlanIO):
         self.use_graph = use_graph
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.device)
+        self.copy_stream = torch.cuda.Stream(device=self.device)
         self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
         # side streams pay off when a launch leaves most SMs idle (few matrices)
         self.multi_stream = True
@@ -390,7 +405,7 @@ class HQREngine(PlanIO):
         streams, cross-stream dependencies as events -- a DAG once captured."""
         torch = self.torch
         if not self.side or not self.multi_stream:
-            self.plan.run(self.stream.cuda_stream)
+            self.plan.run(self.stream.cuda_stream, stop=self._tail)
             return
         self._evs = []
 
@@ -403,22 +418,36 @@ class HQREngine(PlanIO):
         fork.record(self.stream)
         for st in self.side:
             st.wait_event(fork)
-        self.plan.run(self.stream.cuda_stream, [self.stream] + self.side, mk)
+        self.plan.run(self.stream.cuda_stream, [self.stream] + self.side, mk, stop=self._tail)
 
-    def execute(self):
-        """Run the factorization on the device (graph replay when captured)."""
+    def execute(self, tail: bool = True):
+        """Run the factorization on the device (graph replay when captured);
+        tail=False leaves the output compaction of a stream_out engine to
+        launch_tail()."""
         torch = self.torch
         if not self.use_graph:
             self._launch()
+        else:
+            if self.graph is None:
+                self.stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._launch()
+                self.graph = g
+            with torch.cuda.stream(self.stream):
+                self.graph.replay()
+        if tail:
+            self.launch_tail()
+
+    def launch_tail(self):
+        """stream_out: the output compaction, outside the graph -- it
+        overwrites the output region only once the previous run's factors are
+        on the host (event of the last collect's copies)."""
+        if self._tail is None:
             return
-        if self.graph is None:
-            self.stream.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=self.stream):
-                self._launch()
-            self.graph = g
-        with torch.cuda.stream(self.stream):
-            self.graph.replay()
+        if self._d2h_done is not None:
+            self.stream.wait_event(self._d2h_done)
+        self.plan._launch_list(self.plan.launch[self._tail:], self.stream.cuda_stream, _abi.load())
 
     def download(self):
         """D2H of the rank table and the compact factor stream."""
@@ -452,14 +481,41 @@ class HQREngine(PlanIO):
         """pack (worker threads) -> H2D per matrix as its range is packed ->
         graph replay -> rank table D2H -> per-matrix D2H of the compact factors,
         each matrix assembled on a worker thread as soon as its copy lands."""
-        self.submit(mats)
-        return self.collect()
+        return self.collect(self.submit(mats))
+
+    def factorize_stream(self, batches):
+        """Factor a sequence of batches, yielding each batch's factors: batch
+        i+1 is packed, uploaded and launched before batch i's factors are
+        copied back, so (with stream_out) the device-to-host traffic of one
+        batch overlaps the next batch's device work."""
+        if not self.stream_out:   # the output region aliases scratch: no overlap
+            for mats in batches:
+                yield self.factorize(mats)
+            return
+        pending = None
+        for mats in batches:
+            self.launch_main(mats)
+            if pending is not None:
+                out = self.collect(pending)    # copies overlap this batch's graph
+                pending = self.finish()        # its compaction waits for those copies
+                yield out
+            else:
+                pending = self.finish()
+        if pending is not None:
+            yield self.collect(pending)
 
     def submit(self, mats):
         """First half of factorize(): pack, upload and launch; returns as soon
         as the replay is enqueued (the device works while the host goes on)."""
+        self.launch_main(mats)
+        return self.finish()
+
+    def launch_main(self, mats):
+        """pack + H2D + the graph (without a stream_out engine's compaction)."""
         torch = self.torch
         self._tr = [("start", _now())]
+        if getattr(self, "_h2d_done", None) is not None:
+            self._h2d_done.synchronize()   # the staging buffers of the previous run were consumed
         futs = self.pack_async(mats)
         p = self.plan
         with torch.cuda.stream(self.stream):
@@ -472,20 +528,42 @@ class HQREngine(PlanIO):
                 lo, hi = self.in_ranges[b]
                 if hi > lo:
                     self.d_in[lo:hi].copy_(self.h_in[lo:hi], non_blocking=True)
+            self._h2d_done = torch.cuda.Event()
+            self._h2d_done.record(self.stream)
         self._tr.append(("packed", _now()))
-        self.execute()
+        self.execute(tail=False)
+
+    def finish(self):
+        """Output compaction, rank-table read-back and the run's done event;
+        returns the token collect() takes."""
+        torch = self.torch
+        p = self.plan
+        self.launch_tail()
+        par = self._step & 1
+        self._step += 1
+        self.h_rk_out, self.h_tot = self._h_rk_outs[par], self._h_tots[par]
         with torch.cuda.stream(self.stream):
             self.h_tot.copy_(p.totals, non_blocking=True)
             self.h_rk_out.copy_(p.rank, non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(self.stream)
         self._tr.append(("replay_enqueued", _now()))
+        return (done, self.h_rk_out, self.h_tot, self._tr)
 
-    def collect(self):
-        """Second half of factorize(): wait for the run, then D2H + assembly."""
+    def collect(self, token=None):
+        """Second half of factorize(): wait for the run, then D2H + assembly.
+        The copies go on a copy stream, so a run submitted meanwhile keeps
+        computing (factorize_stream)."""
         torch = self.torch
-        tr = self._tr
-        self.stream.synchronize()
+        if token is None:
+            token = (None, self.h_rk_out, self.h_tot, self._tr)
+        done, h_rk, h_tot, tr = token
+        if done is None:
+            self.stream.synchronize()
+        else:
+            done.synchronize()
         tr.append(("device_done", _now()))
-        rk = self.h_rk_out.numpy().copy()
+        rk = h_rk.numpy().copy()
         if int(rk[self.builder.flag_slot]) != 0:
             raise RankCapacityError(f"a truncated rank exceeded the capacity kcap={self.kcap}; "
                                     "retry with a larger kcap")
@@ -494,7 +572,12 @@ class HQREngine(PlanIO):
         self._retune(rk)
         pool = _pool()
         jobs = []
-        with torch.cuda.stream(self.stream):
+        cs = self.copy_stream
+        if done is not None:
+            cs.wait_event(done)
+        else:
+            cs.wait_stream(self.stream)
+        with torch.cuda.stream(cs):
             taken = []
             for b in range(self.B):
                 # each matrix's factors land in their own pinned block, recycled
@@ -505,8 +588,11 @@ class HQREngine(PlanIO):
                 if hi > lo:
                     hb[:hi - lo].copy_(self.d_out[lo:hi], non_blocking=True)
                 ev = torch.cuda.Event()
-                ev.record(self.stream)
+                ev.record(cs)
                 jobs.append(pool.submit(self._assemble, b, ev, rk, offs, hb, lo))
+            d2h = torch.cuda.Event()
+            d2h.record(cs)
+            self._d2h_done = d2h
         tr.append(("d2h_enqueued", _now()))
         out = [j.result() for j in jobs]
         tr.append(("assembled", _now()))

@@ -1036,7 +1036,7 @@ def schedule(builder):
 class CompiledPlan:
     """Ops packed into one device descriptor buffer; run() launches them."""
 
-    def __init__(self, builder: Builder, device):
+    def __init__(self, builder: Builder, device, alias_out: bool = True):
         import torch
         self.b = builder
         self.device = device
@@ -1045,7 +1045,8 @@ class CompiledPlan:
         # the compact output stream is written by the last op only (which joins
         # every lane): it shares the largest scratch region that can hold it
         scratch = [r for r in sizes if r not in (R_PERSIST, R_IN, R_OUT, R_SHARED) and sizes[r] >= sizes.get(R_OUT, 0)]
-        self.out_alias = max(scratch, key=lambda r: sizes[r]) if scratch and sizes.get(R_OUT, 0) > 0 else None
+        self.out_alias = (max(scratch, key=lambda r: sizes[r]) if alias_out and scratch and sizes.get(R_OUT, 0) > 0
+                          else None)
         bases, acc = {}, 0
         for r in sorted(sizes):
             if r == R_OUT and self.out_alias is not None:
@@ -1165,16 +1166,18 @@ class CompiledPlan:
     def launch_one(self, lib, rec, stream_handle):
         self._launch_list([rec], stream_handle, lib)
 
-    def run(self, stream_handle: int, streams=None, events=None):
-        """Launch every op.  With `streams` (torch streams indexed by lane)
-        and an event factory, ops go to their lane's stream and cross-lane
-        dependencies become event waits (DAG under graph capture)."""
+    def run(self, stream_handle: int, streams=None, events=None, stop=None):
+        """Launch every op (the first `stop` ops when given).  With `streams`
+        (torch streams indexed by lane) and an event factory, ops go to their
+        lane's stream and cross-lane dependencies become event waits (DAG
+        under graph capture)."""
         lib = _abi.load()
+        launch = self.launch if stop is None else self.launch[:stop]
         if streams is None or len(streams) == 1:
-            self._launch_list(self.launch, stream_handle, lib)
+            self._launch_list(launch, stream_handle, lib)
             return
         done = {}
-        for i, rec in enumerate(self.launch):
+        for i, rec in enumerate(launch):
             ln = self.lanes[i]
             st = streams[ln]
             for j in self.waits[i]:

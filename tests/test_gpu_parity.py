@@ -86,3 +86,25 @@ def test_gpu_batched_results_independent_and_persistent(hqr_gpu):
         del fb2
     for i in range(3):
         assert np.linalg.norm(snap[i] - snap[i + 1]) > 1e-3 * np.linalg.norm(snap[i])
+
+
+def test_gpu_factorize_stream_matches_factorize(hqr_gpu):
+    """A stream_out engine's factorize_stream (batch i's copies overlapping
+    batch i+1's device work) returns exactly the factors of separate
+    factorize calls, for a sequence of different batches."""
+    from paper_1809_10585_b200.hqr import HQREngine
+    batches = [[gen.gen_random_hodlr(512, 64, 8, 8.0, seed=10 * i + s) for s in range(3)] for i in range(4)]
+    ref_eng = HQREngine(batches[0][0].tree(), 3, 1e-10)
+    ref = [[to_dense(f.r) for f in ref_eng.factorize(bt)] for bt in batches]
+    eng = HQREngine(batches[0][0].tree(), 3, 1e-10, stream_out=True)
+    outs = list(eng.factorize_stream(batches))
+    assert len(outs) == len(batches)
+    for fs, rs in zip(outs, ref):
+        for f, rd in zip(fs, rs):
+            validate_structure(f.r)
+            assert np.array_equal(to_dense(f.r), rd)
+    # and again (graphs captured, pinned blocks recycled)
+    outs2 = list(eng.factorize_stream(batches[::-1]))
+    for fs, rs in zip(outs2, ref[::-1]):
+        for f, rd in zip(fs, rs):
+            assert np.array_equal(to_dense(f.r), rd)
