@@ -7,7 +7,10 @@
 #include "hq_common.cuh"
 
 namespace {
-constexpr int NT = 256, BK = 16;
+#ifndef HQ_GEMM_BK
+#define HQ_GEMM_BK 16
+#endif
+constexpr int NT = 256, BK = HQ_GEMM_BK;
 
 // async 8-byte copy with zero fill when !valid (src-size 0)
 __device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
@@ -631,6 +634,13 @@ extern "C" int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob,
   cudaStream_t st = (cudaStream_t)stream;
   if (tile == 32) {
     constexpr int S = 4, smem = S * BK * (36 + 36) * 8;
+    static bool attr32 = false;
+    if (!attr32) {
+      cudaError_t e = cudaFuncSetAttribute(gemm_kernel<32, 32, 2, 2, S>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return hq_err(e);
+      attr32 = true;
+    }
     gemm_kernel<32, 32, 2, 2, S><<<grid, 128, smem, st>>>(probs, terms, rank, ksplit, skip);
   } else {
     constexpr int S = 3, smem = S * BK * (68 + 68) * 8;
