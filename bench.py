@@ -197,6 +197,7 @@ def instrument(eng, torch):
     s = eng.stream
     per = {}
     eng.upload()
+    eng.stage_to_live()
     s.synchronize()
     evs = []
     orig = plan.launch
@@ -311,7 +312,7 @@ def main():
     per_step = total_batch if total_batch > 1 else ws * len(mats)
     value = per_step * args.steps / (ms / 1e3)
     # ---- end-to-end through the public API with host buffers
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(4, min(2 * args.steps, 10))   # batches in the stream (fill and drain amortised)
     for f in eng.factorize_stream([mats] * 3):  # untimed warm-up: worker pools, pinned result blocks
         pass
     barrier()

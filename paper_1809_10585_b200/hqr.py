@@ -308,7 +308,14 @@ class HQREngine(PlanIO):
         last = self.builder.ops[-1]
         assert last[0] == "pack_copy" and last[2].get("which") == 0, "plan must end with the output compaction"
         self._tail = len(self.plan.launch) - 1 if self.stream_out else None
+        first = self.builder.ops[0]
+        assert first[0] == "pack_copy" and first[2].get("which") == 1, "plan must start with the input restore"
+        # streaming engines also run the input restore outside the graph, so the
+        # next batch's upload can start as soon as it has consumed the inputs
+        self._head = 1 if self.stream_out else 0
         self._d2h_done = None
+        self._consumed = None
+        self._h2d_ready = None
         self._step = 0
         pin = lambda a: torch.from_numpy(a).pin_memory()
         self.h_rk, self.h_sc, self.h_px = pin(self.rk), pin(self.sc), pin(self.px)
@@ -329,11 +336,18 @@ class HQREngine(PlanIO):
         self.d_out = p.arena[ob:ob + out_cap]
         pxo = p.bases[R_PERSIST] + self.builder.PX.off
         self.d_px = p.arena[pxo:pxo + self.px.size]
+        # where a run's rank table / scalars / power start are uploaded to:
+        # the live buffers, or (streaming) staging copied in at execute()
+        if self.stream_out:
+            self._src = (torch.empty_like(p.rank), torch.empty_like(p.scal), torch.empty_like(self.d_px))
+        else:
+            self._src = (p.rank, p.scal, self.d_px)
         self.n_out = 0
         self.use_graph = use_graph
         self.graph = None
         self.stream = torch.cuda.Stream(device=self.device)
         self.copy_stream = torch.cuda.Stream(device=self.device)
+        self.h2d_stream = torch.cuda.Stream(device=self.device)
         self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
         # side streams pay off when a launch leaves most SMs idle (few matrices)
         self.multi_stream = True
@@ -368,12 +382,12 @@ class HQREngine(PlanIO):
 
     def upload(self):
         """H2D of the compact input stream, the rank table and the scalars."""
-        p = self.plan
+        rk, sc, px = self._src
         with self.torch.cuda.stream(self.stream):
             self.d_in[:self.n_in].copy_(self.h_in[:self.n_in], non_blocking=True)
-            p.rank.copy_(self.h_rk, non_blocking=True)
-            p.scal.copy_(self.h_sc, non_blocking=True)
-            self.d_px.copy_(self.h_px, non_blocking=True)
+            rk.copy_(self.h_rk, non_blocking=True)
+            sc.copy_(self.h_sc, non_blocking=True)
+            px.copy_(self.h_px, non_blocking=True)
 
     def h2d_bytes(self):
         return 8 * (self.n_in + self.px.size + self.sc.size) + 4 * self.rk.size
@@ -385,19 +399,20 @@ class HQREngine(PlanIO):
         """Re-arm a run with the input already resident in HBM (device-side
         restore of the rank table / power start; the compact input stream in
         HBM is untouched by a run)."""
-        p = self.plan
+        rk, sc, px = self._src
         with self.torch.cuda.stream(self.stream):
-            p.rank.copy_(self.d_rk0, non_blocking=True)
-            p.scal.copy_(self.d_sc0, non_blocking=True)
-            self.d_px.copy_(self.d_px0, non_blocking=True)
+            rk.copy_(self.d_rk0, non_blocking=True)
+            sc.copy_(self.d_sc0, non_blocking=True)
+            px.copy_(self.d_px0, non_blocking=True)
 
     def snapshot_device_input(self):
         """Keep a device copy of the freshly uploaded run state (call after
         upload(), before execute())."""
+        rk, sc, px = self._src
         with self.torch.cuda.stream(self.stream):
-            self.d_rk0 = self.plan.rank.clone()
-            self.d_sc0 = self.plan.scal.clone()
-            self.d_px0 = self.d_px.clone()
+            self.d_rk0 = rk.clone()
+            self.d_sc0 = sc.clone()
+            self.d_px0 = px.clone()
 
     def _launch(self):
         """Issue the plan: the critical chain on the engine stream, off-chain
@@ -405,7 +420,7 @@ class HQREngine(PlanIO):
         streams, cross-stream dependencies as events -- a DAG once captured."""
         torch = self.torch
         if not self.side or not self.multi_stream:
-            self.plan.run(self.stream.cuda_stream, stop=self._tail)
+            self.plan.run(self.stream.cuda_stream, stop=self._tail, start=self._head)
             return
         self._evs = []
 
@@ -418,13 +433,24 @@ class HQREngine(PlanIO):
         fork.record(self.stream)
         for st in self.side:
             st.wait_event(fork)
-        self.plan.run(self.stream.cuda_stream, [self.stream] + self.side, mk, stop=self._tail)
+        self.plan.run(self.stream.cuda_stream, [self.stream] + self.side, mk, stop=self._tail, start=self._head)
 
     def execute(self, tail: bool = True):
         """Run the factorization on the device (graph replay when captured);
         tail=False leaves the output compaction of a stream_out engine to
         launch_tail()."""
         torch = self.torch
+        if self.stream_out:
+            # streaming head: the staged run state goes live, then the input
+            # restore (the compact input stream is free once it has run)
+            p = self.plan
+            if self._h2d_ready is not None:
+                self.stream.wait_event(self._h2d_ready)
+                self._h2d_ready = None
+            self.stage_to_live()
+            p._launch_list(p.launch[:self._head], self.stream.cuda_stream, _abi.load())
+            self._consumed = torch.cuda.Event()
+            self._consumed.record(self.stream)
         if not self.use_graph:
             self._launch()
         else:
@@ -438,6 +464,16 @@ class HQREngine(PlanIO):
                 self.graph.replay()
         if tail:
             self.launch_tail()
+
+    def stage_to_live(self):
+        """Streaming engines: copy the staged rank table / scalars / power
+        start into the buffers the kernels use (engine stream)."""
+        p = self.plan
+        if self._src[0] is p.rank:
+            return
+        with self.torch.cuda.stream(self.stream):
+            for live, src in zip((p.rank, p.scal, self.d_px), self._src):
+                live.copy_(src, non_blocking=True)
 
     def launch_tail(self):
         """stream_out: the output compaction, outside the graph -- it
@@ -517,11 +553,14 @@ class HQREngine(PlanIO):
         if getattr(self, "_h2d_done", None) is not None:
             self._h2d_done.synchronize()   # the staging buffers of the previous run were consumed
         futs = self.pack_async(mats)
-        p = self.plan
-        with torch.cuda.stream(self.stream):
-            p.rank.copy_(self.h_rk, non_blocking=True)
-            p.scal.copy_(self.h_sc, non_blocking=True)
-            self.d_px.copy_(self.h_px, non_blocking=True)
+        up = self.h2d_stream if self.stream_out else self.stream
+        if self.stream_out and self._consumed is not None:
+            up.wait_event(self._consumed)   # the previous run's restore read the input region
+        rk, sc, px = self._src
+        with torch.cuda.stream(up):
+            rk.copy_(self.h_rk, non_blocking=True)
+            sc.copy_(self.h_sc, non_blocking=True)
+            px.copy_(self.h_px, non_blocking=True)
             for b, fs in enumerate(futs):
                 for f in fs:
                     f.result()
@@ -529,7 +568,9 @@ class HQREngine(PlanIO):
                 if hi > lo:
                     self.d_in[lo:hi].copy_(self.h_in[lo:hi], non_blocking=True)
             self._h2d_done = torch.cuda.Event()
-            self._h2d_done.record(self.stream)
+            self._h2d_done.record(up)
+            if self.stream_out:
+                self._h2d_ready = self._h2d_done
         self._tr.append(("packed", _now()))
         self.execute(tail=False)
 

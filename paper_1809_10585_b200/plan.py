@@ -1166,22 +1166,24 @@ class CompiledPlan:
     def launch_one(self, lib, rec, stream_handle):
         self._launch_list([rec], stream_handle, lib)
 
-    def run(self, stream_handle: int, streams=None, events=None, stop=None):
-        """Launch every op (the first `stop` ops when given).  With `streams`
-        (torch streams indexed by lane) and an event factory, ops go to their
-        lane's stream and cross-lane dependencies become event waits (DAG
-        under graph capture)."""
+    def run(self, stream_handle: int, streams=None, events=None, stop=None, start=0):
+        """Launch ops start..stop-1 (all by default).  With `streams` (torch
+        streams indexed by lane) and an event factory, ops go to their lane's
+        stream and cross-lane dependencies become event waits (DAG under graph
+        capture); ops before `start` ran on the origin stream beforehand."""
         lib = _abi.load()
-        launch = self.launch if stop is None else self.launch[:stop]
+        end = len(self.launch) if stop is None else stop
         if streams is None or len(streams) == 1:
-            self._launch_list(launch, stream_handle, lib)
+            self._launch_list(self.launch[start:end], stream_handle, lib)
             return
         done = {}
-        for i, rec in enumerate(launch):
+        for i in range(start, end):
+            rec = self.launch[i]
             ln = self.lanes[i]
             st = streams[ln]
             for j in self.waits[i]:
-                st.wait_event(done[j])
+                if j >= start:
+                    st.wait_event(done[j])
             self._launch_list([rec], st.cuda_stream, lib)
             if i in self.signal:
                 ev = events()
