@@ -556,7 +556,33 @@ __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __res
       const double* ap0 = T.a + (size_t)r0 * T.lda;
       const size_t rstep = (size_t)(NT / 32) * T.lda;
       const int nq = min(RQ, (m - 1 - r0) / (NT / 32) + 1);
-      for (int k = kb + lane; k < ke; k += 32) {
+      // two k steps per iteration: 2 x (RQ + NC) independent loads in flight
+      int k = kb + lane;
+      for (; k + 32 < ke; k += 64) {
+        double b[2][NC], av[2][RQ];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kk = k + 32 * h;
+#pragma unroll
+          for (int j = 0; j < NC; ++j) {
+            const int jj = j < n ? j : 0;
+            const double v = __ldg(T.b + (size_t)kk * sbk + jj * sbj);
+            b[h][j] = plain ? v : hq_mask(v, T.tb == 0 ? kk : jj, T.tb == 0 ? jj : kk, T.mask_b);
+          }
+#pragma unroll
+          for (int q = 0; q < RQ; ++q) {
+            const double v = __ldg(ap0 + (q < nq ? q * rstep : 0) + kk);
+            av[h][q] = plain ? v : hq_mask(v, kk, r0 + (NT / 32) * q, T.mask_a);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < RQ; ++q)
+#pragma unroll
+            for (int j = 0; j < NC; ++j) d[q][j] = fma(av[h][q], b[h][j], d[q][j]);
+      }
+      for (; k < ke; k += 32) {
         double b[NC];
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
