@@ -85,3 +85,36 @@ def test_tsqr_path_for_tall_factor_stacks(monkeypatch):
     assert np.linalg.norm(to_dense(f.r) - to_dense(r)) <= 1e-8 * np.linalg.norm(to_dense(r))
     e_orth, e_acc = O.dense_metrics(to_dense(a), f.y, f.t, f.r)
     assert e_orth <= 1e-13 and e_acc <= 1e-11
+
+
+def test_svd_cluster_sizes_from_runtime_sizes():
+    """Cluster choice of a Jacobi launch (plan.svd_cluster_runtime): tiny
+    cores stay on one CTA, a core goes to the smallest cluster whose shared
+    memory holds it, widened while the launch fits one wave of 148 SMs."""
+    from paper_1809_10585_b200.plan import _svd_fits, svd_cluster_runtime
+    assert svd_cluster_runtime(1, 24, 24) == 1            # few pairs: one SM
+    assert svd_cluster_runtime(1, 200, 200) == 8           # one core: widest cluster
+    assert svd_cluster_runtime(32, 200, 200) == 4          # 32 x 4 CTAs = one wave
+    assert svd_cluster_runtime(64, 120, 120) == 2
+    assert svd_cluster_runtime(64, 600, 300) == 1          # beyond the cluster path (m > 512)
+    for G in (2, 4, 8):
+        n = 8
+        while _svd_fits(G, n + 8, n + 8):
+            n += 8
+        assert svd_cluster_runtime(1000, n, n) == G        # many problems: the smallest fitting cluster
+
+
+def test_retune_clusters_uses_the_rank_table():
+    """After a run the Jacobi launches are re-sized from the core sizes in the
+    rank table (not the capacities), and only the svd ops change."""
+    from paper_1809_10585_b200.plan import retune_clusters
+    a = gen.gen_random_hodlr(1024, 128, 16, 8.0, seed=0)
+    (f,), io, plan = emulate([a], 1e-10)
+    rk = plan.rank.numpy().copy()
+    before = [dict(ex) for _, _, ex in io.builder.ops]
+    retune_clusters(io.builder, rk)
+    for (kind, probs, ex), old in zip(io.builder.ops, before):
+        if kind != "svd":
+            assert ex == old
+        else:
+            assert ex["cluster"] in (1, 2, 4, 8)

@@ -32,9 +32,27 @@ for ta in (0, 1):
         probs[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, 7 * p, 7, 0, 0.0)
     dt, dp = put(terms), put(probs)
     nbytes = (L.numel() + U.numel()) * 8
-    for mode in (0, 1, 2):
+    for mode in ((0, 1, 2, 3) if ta == 0 else (0, 1, 2, 4)):
         us = timeit(lambda: lib.hq_gemm_skinny(None, dp.data_ptr(), P, dt.data_ptr(), rank.data_ptr(), 1, 2, mode, 256, None))
         print(f"leaf phase P={P} ta={ta} mode {mode}: {us:8.1f} us  {nbytes / us / 1e3:7.1f} GB/s", flush=True)
+# split of the mixed A^T leaf phase: leaf term alone (mode 4) + low-rank terms alone (mode 3)
+L = torch.randn(P, 256 * 256, dtype=torch.float64, device="cuda")
+U = torch.randn(P, 6, 256 * 16, dtype=torch.float64, device="cuda")
+X = torch.randn(P, 512, dtype=torch.float64, device="cuda")
+T = torch.randn(P, 6, 32, dtype=torch.float64, device="cuda")
+C = torch.zeros(P, 512, dtype=torch.float64, device="cuda")
+t1 = np.zeros(P, _abi.GEMM_TERM); p1 = np.zeros(P, _abi.GEMM_PROB)
+t2 = np.zeros(P * 6, _abi.GEMM_TERM); p2 = np.zeros(P, _abi.GEMM_PROB)
+for p in range(P):
+    t1[p] = (L[p].data_ptr(), X[p].data_ptr(), 256, 256, 1, 0, 256, -1, 0, 0, 1.0)
+    p1[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, p, 1, 0, 0.0)
+    for q in range(6):
+        t2[6 * p + q] = (U[p, q].data_ptr(), T[p, q].data_ptr(), 256, 16, 0, 0, 16, -1, 0, 0, 1.0)
+    p2[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, 6 * p, 6, 0, 1.0)
+d1, q1, d2, q2 = put(t1), put(p1), put(t2), put(p2)
+us1 = timeit(lambda: lib.hq_gemm_skinny(None, q1.data_ptr(), P, d1.data_ptr(), rank.data_ptr(), 1, 2, 4, 256, None))
+us2 = timeit(lambda: lib.hq_gemm_skinny(None, q2.data_ptr(), P, d2.data_ptr(), rank.data_ptr(), 1, 2, 3, 256, None))
+print(f"split A^T leaf phase P={P}: leaf-only mode 4 {us1:8.1f} us ({L.numel() * 8 / us1 / 1e3:.0f} GB/s) + lowrank mode 3 {us2:8.1f} us ({U.numel() * 8 / us2 / 1e3:.0f} GB/s) = {us1 + us2:8.1f} us", flush=True)
 # V^T X phase: rank 16 rows, K = 8192 .. 256 (2 blocks per node, 2**l nodes)
 for K, cnt in ((8192, 2), (4096, 4), (1024, 16), (256, 64)):
     Pp = cnt * 8
