@@ -29,14 +29,30 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile the three translation units in parallel (objects in a
+    temporary directory), then link the shared library."""
+    import tempfile
     if not force and not stale():
         return LIB
     extra = os.environ.get("HQ_EXTRA_FLAGS", "").split()
     out = os.environ.get("HQ_LIB_OUT", LIB)
-    cmd = [nvcc()] + FLAGS + extra + ["-o", out] + [os.path.join(CSRC, s) for s in SOURCES]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True)
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+    with tempfile.TemporaryDirectory(prefix="hqb200-build-") as tmp:
+        objs, procs = [], []
+        for src in SOURCES:
+            obj = os.path.join(tmp, src.replace(".cu", ".o"))
+            cmd = [nvcc()] + compile_flags + extra + ["-c", "-o", obj, os.path.join(CSRC, src)]
+            if verbose:
+                print(" ".join(cmd))
+            procs.append((subprocess.Popen(cmd), cmd))
+            objs.append(obj)
+        for proc, cmd in procs:
+            if proc.wait() != 0:
+                raise subprocess.CalledProcessError(proc.returncode, cmd)
+        link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out] + objs
+        if verbose:
+            print(" ".join(link))
+        subprocess.run(link, check=True)
     return out
 
 
