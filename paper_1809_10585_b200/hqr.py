@@ -12,7 +12,6 @@ without a CUDA device or the library this raises.
 
 from __future__ import annotations
 
-import math
 import os
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
@@ -21,7 +20,7 @@ from functools import lru_cache
 import numpy as np
 
 from . import _abi
-from .hodlr import (GENERAL, UNIT_LOWER_TRIANGULAR, UPPER_TRIANGULAR, HodlrMatrix, LowRankBlock,
+from .hodlr import (UNIT_LOWER_TRIANGULAR, UPPER_TRIANGULAR, HodlrMatrix, LowRankBlock,
                     PartitionTree)
 from .plan import R_IN, R_OUT, R_PERSIST, Builder, CompiledPlan, retune_clusters
 
