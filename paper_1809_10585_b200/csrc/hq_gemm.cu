@@ -339,12 +339,12 @@ __global__ void __launch_bounds__(NT) gemm_rows_kernel(const hq_gemm_prob* __res
 //               k, warp-shuffle reduction, shared-memory accumulation.
 // B (k x NC) is tiny and read through the cache.  K-split slices add into C
 // atomically (the caller zeroed C).
-constexpr int GV_ROWS = 64, GV_U = 8, GV_RQ = GV_ROWS / (NT / 32);
+constexpr int GV_ROWS = 64, GV_U = 8, GV_RQ = GV_ROWS / (NT / 32), GV_RQH = 4;
 // KIND 0: terms of both layouts; 1: only op(A) = A; 2: only op(A) = A^T
 // (the planner knows each launch's layouts; the lean variants keep fewer
 // registers live and run more warps per SM)
 template <int NC, int KIND>
-__global__ void __launch_bounds__(NT, KIND == 1 ? 3 : 2) gemv_kernel(const hq_gemm_prob* __restrict__ probs,
+__global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm_prob* __restrict__ probs,
                                                   const hq_gemm_term* __restrict__ terms,
                                                   const int* __restrict__ rank, int ksplit,
                                                   const int* __restrict__ skip) {
@@ -433,48 +433,52 @@ __global__ void __launch_bounds__(NT, KIND == 1 ? 3 : 2) gemv_kernel(const hq_ge
       // step issues one load per row (independent) plus the B loads
       const int sub = wid % wpr, ngrp = (NT / 32) / wpr, r0 = wid / wpr;
       const int st = 32 * wpr;
-      double d[GV_RQ][NC];
-#pragma unroll
-      for (int q = 0; q < GV_RQ; ++q)
-#pragma unroll
-        for (int j = 0; j < NC; ++j) d[q][j] = 0.0;
       // rows past nr re-read row r0 (their sums are dropped)
       const double* ap0 = T.a + (size_t)(i0 + r0) * T.lda;
       const size_t rstep = (size_t)ngrp * T.lda;
       const int nq = r0 < nr ? (nr - 1 - r0) / ngrp + 1 : 0;   // valid rows of this warp
-      bool rv[GV_RQ];
+      // the rows go in chunks of GV_RQH (fewer live registers: more warps per SM)
+      for (int qc = 0; qc < nq; qc += GV_RQH) {
+        double d[GV_RQH][NC];
 #pragma unroll
-      for (int q = 0; q < GV_RQ; ++q) rv[q] = q < nq;
-      if (plain) {
-        for (int k = kb + sub * 32 + lane; k < ke; k += st) {
-          double b[NC], a[GV_RQ];
+        for (int q = 0; q < GV_RQH; ++q)
 #pragma unroll
-          for (int j = 0; j < NC; ++j) b[j] = __ldg(T.b + (size_t)k * sbk + bj[j]);
+          for (int j = 0; j < NC; ++j) d[q][j] = 0.0;
+        bool rv[GV_RQH];
 #pragma unroll
-          for (int q = 0; q < GV_RQ; ++q) a[q] = __ldg(ap0 + (rv[q] ? q * rstep : 0) + k);
+        for (int q = 0; q < GV_RQH; ++q) rv[q] = qc + q < nq;
+        const double* apc = ap0 + (size_t)qc * rstep;
+        if (plain) {
+          for (int k = kb + sub * 32 + lane; k < ke; k += st) {
+            double b[NC], a[GV_RQH];
 #pragma unroll
-          for (int q = 0; q < GV_RQ; ++q)
+            for (int j = 0; j < NC; ++j) b[j] = __ldg(T.b + (size_t)k * sbk + bj[j]);
 #pragma unroll
-            for (int j = 0; j < NC; ++j) d[q][j] = fma(a[q], b[j], d[q][j]);
-        }
-      } else {
-        for (int k = kb + sub * 32 + lane; k < ke; k += st) {
+            for (int q = 0; q < GV_RQH; ++q) a[q] = __ldg(apc + (rv[q] ? q * rstep : 0) + k);
 #pragma unroll
-          for (int q = 0; q < GV_RQ; ++q) {
-            if (!rv[q]) continue;
-            const double a = hq_mask(ap0[q * rstep + k], k, i0 + r0 + ngrp * q, T.mask_a);
+            for (int q = 0; q < GV_RQH; ++q)
 #pragma unroll
-            for (int j = 0; j < NC; ++j) d[q][j] = fma(a, bval(k, j), d[q][j]);
+              for (int j = 0; j < NC; ++j) d[q][j] = fma(a[q], b[j], d[q][j]);
+          }
+        } else {
+          for (int k = kb + sub * 32 + lane; k < ke; k += st) {
+#pragma unroll
+            for (int q = 0; q < GV_RQH; ++q) {
+              if (!rv[q]) continue;
+              const double a = hq_mask(apc[q * rstep + k], k, i0 + r0 + ngrp * (qc + q), T.mask_a);
+#pragma unroll
+              for (int j = 0; j < NC; ++j) d[q][j] = fma(a, bval(k, j), d[q][j]);
+            }
           }
         }
-      }
 #pragma unroll
-      for (int q = 0; q < GV_RQ; ++q) {
-        if (!rv[q]) continue;   // warp-uniform
+        for (int q = 0; q < GV_RQH; ++q) {
+          if (!rv[q]) continue;   // warp-uniform
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          const double v = warp_sum(d[q][j]);
-          if (lane == 0) atomicAdd(&dotr[r0 + ngrp * q][j], T.alpha * v);
+          for (int j = 0; j < NC; ++j) {
+            const double v = warp_sum(d[q][j]);
+            if (lane == 0) atomicAdd(&dotr[r0 + ngrp * (qc + q)][j], T.alpha * v);
+          }
         }
       }
     }
