@@ -22,7 +22,7 @@ namespace cg = cooperative_groups;
 namespace {
 constexpr int CNT = 512, CNW = CNT / 32;
 constexpr int C_MAX_BS = 64;          // max columns per block
-constexpr int C_SMEM_DOUBLES = 22528; // 176 KB: 2 buffer sets x 2 blocks
+constexpr int C_SMEM_DOUBLES = 26880; // 210 KB: 2 buffer sets x 2 blocks (the kernel reserves ~224 KB for the single-CTA fallback anyway)
 
 struct CSmem {
   double buf[C_SMEM_DOUBLES];

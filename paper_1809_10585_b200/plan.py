@@ -807,7 +807,7 @@ class Builder:
 # ---------------------------------------------------------------- packing
 
 SVD_SMEM_DOUBLES = 24576   # single-CTA staging capacity (hq_svd_kernel.cuh)
-CLUSTER_BUF_DOUBLES = 22528  # per-CTA block buffers (hq_svd_cluster.cuh)
+CLUSTER_BUF_DOUBLES = 26880  # per-CTA block buffers (hq_svd_cluster.cuh C_SMEM_DOUBLES)
 SVD_SINGLE_MAX_PAIRS = 16     # HQ_SVD_SINGLE_MAX_PAIRS (hq_svd_cluster.cuh)
 
 
@@ -838,7 +838,7 @@ def svd_cluster(svd_probs):
     return dict(cluster=8, max_m=mmax)
 
 
-SVD_C_SMEM_DOUBLES, SVD_C_MAX_BS = 22528, 64   # hq_svd_cluster.cuh C_SMEM_DOUBLES / C_MAX_BS
+SVD_C_SMEM_DOUBLES, SVD_C_MAX_BS = 26880, 64   # hq_svd_cluster.cuh C_SMEM_DOUBLES / C_MAX_BS
 
 
 def _svd_fits(G, m, n):

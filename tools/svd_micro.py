@@ -13,7 +13,7 @@ for n, kind in cases:
     for xf, CL in ((1, 1), (1, 2), (1, 4), (1, 8)):
         MM = n
         ld, bs = (n + 1) // 2 * 2, -(-n // (2 * CL))
-        if CL > 1 and 4 * bs * ld > 22528: continue
+        if CL > 1 and 4 * bs * ld > 26880: continue
         M = np.linalg.qr(C.T)[1] if xf else C
         for rep in range(2):
             dC = torch.tensor(M.T.copy(), device="cuda")
