@@ -578,6 +578,7 @@ __device__ void factor_panel_core(const hq_qr_prob& Q, double* P, int ldp, int r
   else if (rows <= 256) panel_factor_reg<8>(P, ldp, rows, pw, Q.tau + p0, S);
   else if (rows <= 384) panel_factor_reg<12>(P, ldp, rows, pw, Q.tau + p0, S);
   else if (rows <= 512) panel_factor_reg<16>(P, ldp, rows, pw, Q.tau + p0, S);
+  else if (rows <= 768) panel_factor_reg<24>(P, ldp, rows, pw, Q.tau + p0, S);
   else if (rows <= 1024) panel_factor_reg<32>(P, ldp, rows, pw, Q.tau + p0, S);
   else panel_factor_block(P, ldp, rows, pw, Q.tau + p0, S);
   HQ_TMARK(5);
