@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(NT) gemm_rows_kernel(const hq_gemm_prob* __res
 //               k, warp-shuffle reduction, shared-memory accumulation.
 // B (k x NC) is tiny and read through the cache.  K-split slices add into C
 // atomically (the caller zeroed C).
-constexpr int GV_ROWS = 64, GV_U = 8, GV_RQ = GV_ROWS / (NT / 32), GV_RQH = 4;
+constexpr int GV_ROWS = 64, GV_U = 8, GV_RQH = 4;
 // KIND 0: terms of both layouts; 1: only op(A) = A; 2: only op(A) = A^T
 // (the planner knows each launch's layouts; the lean variants keep fewer
 // registers live and run more warps per SM)

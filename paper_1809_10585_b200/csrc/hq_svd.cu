@@ -95,6 +95,10 @@ static int launch_cluster(cudaStream_t st, const hq_svd_prob* probs, int nprob, 
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return (int)e;
+    if (G > 8) {   // 16-CTA clusters are non-portable (opt-in)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return (int)e;
+    }
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
@@ -120,7 +124,8 @@ extern "C" int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* ra
     (void)max_m;  // cores past the cluster's limits run on CTA 0 (kernel-side test)
     if (cluster == 2) return launch_cluster<2>(st, probs, nprob, rank, scal);
     if (cluster <= 4) return launch_cluster<4>(st, probs, nprob, rank, scal);
-    return launch_cluster<8>(st, probs, nprob, rank, scal);
+    if (cluster <= 8) return launch_cluster<8>(st, probs, nprob, rank, scal);
+    return launch_cluster<16>(st, probs, nprob, rank, scal);
   }
   if (!g_svd_attr) {
     cudaError_t e = cudaFuncSetAttribute(svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -29,7 +29,7 @@ struct CSmem {
   double nrm[4][C_MAX_BS];   // squared norms, [set * 2 + slot]
   int col[4][C_MAX_BS];      // global column index per slot (-1: pad)
   double sig_all[1024];
-  int flag[2][8];            // rotation flags of every CTA, by sweep parity
+  int flag[2][16];           // rotation flags of every CTA, by sweep parity
   double2 trash[32];         // sink for the stores of rows past the column end
   int rot;
   int cnt;
@@ -219,6 +219,9 @@ __device__ __noinline__ void svd_cluster_body(const hq_svd_prob& P, int* __restr
         const double2* src = reinterpret_cast<const double2*>(blk(cur, slot));
         double2* dst = reinterpret_cast<double2*>(R->buf + (size_t)(2 * nxt + dslot[slot]) * bs * ld);
         for (int e = t; e < bs * ld / 2; e += CNT) dst[e] = src[e];
+      }
+      for (int slot = 0; slot < 2; ++slot) {
+        CSmem* R = cluster.map_shared_rank(&S, dcta[slot]);
         for (int jj = t; jj < bs; jj += CNT) {
           R->nrm[2 * nxt + dslot[slot]][jj] = S.nrm[2 * cur + slot][jj];
           R->col[2 * nxt + dslot[slot]][jj] = S.col[2 * cur + slot][jj];
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* 
   const int ld = (m + 1) & ~1;
   const int bs = (n + 2 * G - 1) / (2 * G);
   const bool fits_single = (size_t)ld * n <= SMEM_DOUBLES;
-  const bool fits_cluster = m <= 512 && 4 * bs * ld <= C_SMEM_DOUBLES && bs <= C_MAX_BS;
+  const bool fits_cluster = m <= 640 && 4 * bs * ld <= C_SMEM_DOUBLES && bs <= C_MAX_BS;
   if (!fits_cluster || (fits_single && (n + 1) / 2 <= HQ_SVD_SINGLE_MAX_PAIRS)) {
     if (cr == 0) svd_single(P, rank, scal, *reinterpret_cast<SvdSmem*>(smem_raw));
     return;
@@ -332,7 +335,17 @@ __global__ void __launch_bounds__(CNT, 1) svd_cluster_kernel(const hq_svd_prob* 
   // lane-group shape from the pairs per CTA (bs) and the rows (m)
   // (rows per lane E sized to m: lanes past the column end only waste issue
   // slots on the latency-bound rounds)
-  if (bs <= 16 || m > 256) {
+  if constexpr (G == 16) {
+    // 16-CTA clusters carry the widest cores only (m > 256): one lane group of 32 per pair
+    if (m <= 256) svd_cluster_body<G, 32, 8>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 384) svd_cluster_body<G, 32, 12>(P, rank, m, n, thr, S, cluster);
+    else if (m <= 512) svd_cluster_body<G, 32, 16>(P, rank, m, n, thr, S, cluster);
+    else svd_cluster_body<G, 32, 20>(P, rank, m, n, thr, S, cluster);
+    return;
+  }
+  if (m > 512) {
+    svd_cluster_body<G, 32, 20>(P, rank, m, n, thr, S, cluster);
+  } else if (bs <= 16 || m > 256) {
     if (m <= 128) svd_cluster_body<G, 32, 4>(P, rank, m, n, thr, S, cluster);
     else if (m <= 192) svd_cluster_body<G, 32, 6>(P, rank, m, n, thr, S, cluster);
     else if (m <= 256) svd_cluster_body<G, 32, 8>(P, rank, m, n, thr, S, cluster);

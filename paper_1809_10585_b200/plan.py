@@ -847,7 +847,7 @@ def _svd_fits(G, m, n):
     if G == 1:
         return (m + 1) // 2 * 2 * n <= SVD_SMEM_DOUBLES
     bs = -(-n // (2 * G))
-    return m <= 512 and 4 * bs * ((m + 1) // 2 * 2) <= SVD_C_SMEM_DOUBLES and bs <= SVD_C_MAX_BS
+    return m <= 640 and 4 * bs * ((m + 1) // 2 * 2) <= SVD_C_SMEM_DOUBLES and bs <= SVD_C_MAX_BS
 
 
 def svd_cluster_runtime(nprob, m, n, sms=148):
@@ -861,7 +861,8 @@ def svd_cluster_runtime(nprob, m, n, sms=148):
         return 1
     fit = [G for G in (2, 4, 8) if _svd_fits(G, m, n)]
     if not fit:
-        return 1
+        # too wide for 8 CTAs: a (non-portable) 16-CTA cluster if it fits there
+        return 16 if _svd_fits(16, m, n) else 1
     G = fit[0]
     while G < 8 and nprob * 2 * G <= sms:
         G *= 2

@@ -96,7 +96,8 @@ def test_svd_cluster_sizes_from_runtime_sizes():
     assert svd_cluster_runtime(1, 200, 200) == 8           # one core: widest cluster
     assert svd_cluster_runtime(32, 200, 200) == 4          # 32 x 4 CTAs = one wave
     assert svd_cluster_runtime(64, 120, 120) == 2
-    assert svd_cluster_runtime(64, 600, 300) == 1          # beyond the cluster path (m > 512)
+    assert svd_cluster_runtime(64, 700, 300) == 1          # beyond the cluster path (m > 640)
+    assert svd_cluster_runtime(1, 440, 440) == 16          # too wide for 8 CTAs: a 16-CTA cluster
     for G in (2, 4, 8):
         n = 8
         while _svd_fits(G, n + 8, n + 8):

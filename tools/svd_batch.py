@@ -23,7 +23,7 @@ for n in ns:
             p[i] = (dC[i].data_ptr(), dU[i].data_ptr(), dW[i].data_ptr(), n, n, n, -1, n, -1, n, 4 * i, -1, -1, 1e-10, 1, 0)
         dp = torch.tensor(np.frombuffer(p.tobytes(), np.uint8), device="cuda")
         res = []
-        for CL in (1, 2, 4, 8):
+        for CL in (1, 2, 4, 8, 16):
             best = 1e9
             for rep in range(3):
                 for i in range(P):
