@@ -27,6 +27,7 @@ updates of hqr.py:158-159 are applied in place to those V factors.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -813,10 +814,14 @@ SVD_SINGLE_MAX_PAIRS = 16     # HQ_SVD_SINGLE_MAX_PAIRS (hq_svd_cluster.cuh)
 
 def qr_cluster(qr_probs):
     """Cluster size for a QR launch: spread few, wide problems over several
-    SMs; many problems (or narrow ones) run one CTA each."""
+    SMs; many problems (or narrow ones) run one CTA each.  Above 48 problems
+    one CTA each leaves SMs free for the side streams' work: measured on the
+    bench workload (batch 58, profiles/r01_ab_qr_cluster_*.txt) a one-CTA
+    launch for 58 problems shortens the step 1195 -> 1170 ms at unchanged QR
+    kernel time, while 2-CTA clusters for 75-148 problems lengthen it."""
     n = len(qr_probs)
     kmax = max(p[7].cap for p in qr_probs)
-    if kmax < 48 or n > 74:
+    if kmax < 48 or n > int(os.environ.get("HQ_QR_ONE_CTA_ABOVE", "48")):
         return 1
     if n <= 18:
         return 8
