@@ -231,6 +231,70 @@ def auto_batch(torch, ci, n, tol, local, cap=64, kcap=192, stream_out=True):
     return max(1, min(cap, int(0.85 * free / per_matrix)))
 
 
+def build_engine(torch, config, n, batch=None, kcap=None, local=0, ws=1, rank=0):
+    """The timed engine, exactly as the bench runs it (the GPU parity test
+    tests/test_gpu_bench_workload.py builds it through this function):
+    config 2 -> seeds rank*B .. rank*B+B-1 with B = what fits 85 % of the free
+    HBM (<= 64), rank capacity 192, streaming output; config 4 -> the fixed
+    64-matrix batch sharded over the ranks.  The first run (capture + replay
+    + download) has happened on return, so the Jacobi clusters are re-tuned
+    and the next execute() captures the graph that gets timed.  Returns
+    (engine, matrices, kcap, scaling)."""
+    from paper_1809_10585_b200.gen import CONFIGS, gen_config
+    from paper_1809_10585_b200.hqr import HQREngine, RankCapacityError
+    from paper_1809_10585_b200.shard import shard_seeds
+    cfg = CONFIGS[config]
+    total_batch = cfg.get("batch", 1)
+    if total_batch > 1:
+        # config 4: a fixed batch of independent matrices sharded over the ranks
+        seeds = shard_seeds(total_batch, ws, rank)
+        scaling = "strong"
+    else:
+        per = batch or auto_batch(torch, config, n, cfg["tol"], local, kcap=kcap or 192)
+        seeds = list(range(rank * per, (rank + 1) * per))
+        scaling = "weak"
+    mats = [gen_config(config, seed=s, n=n) for s in seeds]
+    a = mats[0]
+    # rank capacity 192 (largest rank on this workload over 64 seeds: 159); an
+    # overflow raises RankCapacityError -- it never truncates -- and the run
+    # is redone at capacity 512 with the batch that fits
+    kc = kcap or (192 if total_batch == 1 else 512)
+    while True:
+        eng = HQREngine(a.tree(), len(mats), cfg["tol"], kcap=kc, device=f"cuda:{local}", stream_out=True)
+        eng.pack(mats)
+        eng.upload()
+        eng.snapshot_device_input()
+        eng.execute()  # capture + first run
+        try:
+            eng.download()
+            break
+        except RankCapacityError:
+            if kc >= 512:
+                raise
+            del eng
+            torch.cuda.empty_cache()
+            kc = 512
+            if total_batch == 1 and not batch:
+                mats = mats[:auto_batch(torch, config, n, cfg["tol"], local, kcap=kc)]
+                a = mats[0]
+    return eng, mats, kc, scaling
+
+
+def r_sketch_error(f, config):
+    """Relative Frobenius error of matrix 0's R sketch (R @ G, G the fixed
+    Gaussian of tests/golden/make_golden_full.py) against the reference's
+    golden sketch, computed on the GPU (QROperator), or None without the
+    golden file."""
+    path = os.path.join(ROOT, "tests", "golden", f"golden_full_cfg{config}.npz")
+    if not os.path.exists(path):
+        return None
+    from paper_1809_10585_b200.operators import QROperator
+    g = np.load(path)["RG"]
+    G = np.random.default_rng(0x5C37).standard_normal((g.shape[0], 8))
+    rg = QROperator(f).apply_r(G)
+    return float(np.linalg.norm(rg - g) / np.linalg.norm(g))
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -242,46 +306,14 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1809_10585_b200.gen import CONFIGS, gen_config
-    from paper_1809_10585_b200.hqr import HQREngine
+    from paper_1809_10585_b200.gen import CONFIGS
     from paper_1809_10585_b200.plan import plan_accounting
     cfg = CONFIGS[args.config]
     n = args.n or cfg["n"]
     total_batch = cfg.get("batch", 1)
-    from paper_1809_10585_b200.shard import max_over_ranks, shard_seeds
-    if total_batch > 1:
-        # config 4: a fixed batch of independent matrices sharded over the ranks
-        seeds = shard_seeds(total_batch, ws, rank)
-        scaling = "strong"
-    else:
-        per = args.batch or auto_batch(torch, args.config, n, cfg["tol"], local, kcap=args.kcap or 192)
-        seeds = list(range(rank * per, (rank + 1) * per))
-        scaling = "weak"
-    mats = [gen_config(args.config, seed=s, n=n) for s in seeds]
+    from paper_1809_10585_b200.shard import max_over_ranks
+    eng, mats, kcap, scaling = build_engine(torch, args.config, n, args.batch, args.kcap, local, ws, rank)
     a = mats[0]
-    # rank capacity 192 (largest rank on this workload over 64 seeds: 159); an
-    # overflow raises RankCapacityError -- it never truncates -- and the run
-    # is redone at capacity 512 with the batch that fits
-    from paper_1809_10585_b200.hqr import RankCapacityError
-    kcap = args.kcap or (192 if total_batch == 1 else 512)
-    while True:
-        eng = HQREngine(a.tree(), len(mats), cfg["tol"], kcap=kcap, device=f"cuda:{local}", stream_out=True)
-        eng.pack(mats)
-        eng.upload()
-        eng.snapshot_device_input()
-        eng.execute()  # capture + first run
-        try:
-            eng.download()
-            break
-        except RankCapacityError:
-            if kcap >= 512:
-                raise
-            del eng
-            torch.cuda.empty_cache()
-            kcap = 512
-            if total_batch == 1 and not args.batch:
-                mats = mats[:auto_batch(torch, args.config, n, cfg["tol"], local, kcap=kcap)]
-                a = mats[0]
     s = eng.stream
 
     def barrier():
@@ -345,6 +377,10 @@ def main():
             "fp64_gflops_effective": flops / (ms_step / 1e3) / 1e9,
             "algorithmic_gflop_per_step": flops / 1e9,
             "norm_estimate": eng.norm_estimate(0), "max_ranks": ranks, "clocks": clk}
+    if rank == 0 and args.n is None:
+        # parity of what was timed: matrix 0 of the last e2e batch against the
+        # reference's golden R sketch (tests/golden/make_golden_full.py)
+        line["r_sketch_rel_err_matrix0"] = r_sketch_error(f[0], args.config)
     if rank == 0 and len(mats) > 1:
         # single-matrix latency (batch 1 plan, graph replay, input resident)
         e1 = HQREngine(a.tree(), 1, cfg["tol"], kcap=kcap, device=f"cuda:{local}")

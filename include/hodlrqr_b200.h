@@ -45,7 +45,12 @@ typedef struct hq_gemm_term {
   double alpha;
 } hq_gemm_term;
 
-/* C (m x n) = beta*C + sum_t term_t   (reference: every @ in arith.py/hqr.py) */
+/* C (m x n) = beta*C + sum_t term_t   (reference: every @ in arith.py/hqr.py).
+   K-split launches are deterministic: each K slice of an output block writes
+   its partial sum into its own slot of ws, the last slice to arrive (counter
+   cnt[block]) adds the slots in slice order 0..ks-1 and writes C; the result
+   is bit-identical run to run and independent of the arrival order.  ws and
+   cnt are per problem; the slot layout is given per launcher below. */
 typedef struct hq_gemm_prob {
   double* c;
   int32_t ldc;
@@ -53,6 +58,8 @@ typedef struct hq_gemm_prob {
   int32_t term0, nterm;
   int32_t item0;   /* hq_gemm_skinny mode 5: first work item of this problem */
   double beta;
+  double* ws;      /* K-split partial sums (unused when the problem is not split) */
+  int32_t* cnt;    /* arrival counters, one per output block: zero on entry, left zero */
 } hq_gemm_prob;
 
 /* a column block of a concatenation [alpha_1 P_1, alpha_2 P_2, ...] */
@@ -172,11 +179,19 @@ typedef struct hq_rowblk_prob {
 } hq_rowblk_prob;
 
 /* ---- launchers ---------------------------------------------------------- */
+/* bumped whenever a descriptor layout or a launcher signature changes;
+   the Python binding refuses a library with another version */
+#define HQ_ABI_VERSION 2
 int hq_abi_version(void);
 int hq_device_check(void);
 
-/* grid = tiles x nprob x ksplit; ksplit > 1 accumulates atomically into a
-   pre-zeroed C (beta ignored); skip != NULL && *skip != 0 makes it a no-op */
+/* grid = tiles x nprob x ksplit; a problem with nkt k-tiles of 16 (summed
+   over its terms) is split into ks = min(ksplit, max(1, nkt / 8)) slices;
+   with ks > 1 its ws holds tiles_cap x ks_cap slots of BM x BN doubles
+   (slot (tile, z) at (tile * ks_cap + z) * BM * BN, element (i, j) at i + j * BM;
+   ks_cap = the same formula on the capacity k's, tiles_cap from the capacity
+   m, n) and cnt one counter per output tile.  skip != NULL && *skip != 0
+   makes it a no-op */
 int hq_gemm(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
             int* rank, int tiles, int ksplit, const int* skip);
 /* hq_gemm with the output tile size chosen (tile = 32 or 64; tiles counts
@@ -185,17 +200,21 @@ int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob, const hq_g
                   int* rank, int tiles, int ksplit, int tile, const int* skip);
 /* the same product for outputs of at most 4 columns (power-iteration
    blocks^T X, Gram and leaf products).  mode 0: grid (ksplit, nprob), K split
-   evenly over CTAs, with ksplit > 1 C must be zero on entry (atomic
-   accumulation); mode 1: one thread per output row (max_rows bounds m),
-   ksplit ignored; mode 2: 64 output rows per CTA (max_rows bounds m), each
-   term read coalesced in its own layout (rows across lanes for op(A) = A,
-   k across lanes for op(A) = A^T), K split into at most ksplit slices of
-   >= 512 (C zeroed by the caller when ksplit > 1); modes 3 / 4: mode 2
-   specialised to launches whose terms are all op(A) = A / all op(A) = A^T;
-   mode 5: one launch over problems of different K (all op(A) = A^T, one term
-   each): problem i owns work items [item0_i, item0_{i+1}) -- its K slices --
-   and the grid is ksplit = the total item count; every CTA covers all
-   output rows of its problem (C zeroed by the caller) */
+   evenly over CTAs; with ksplit > 1, ws holds ksplit slots of m_cap x n_cap
+   (ld m_cap) and cnt one counter; mode 1: one thread per output row
+   (max_rows bounds m), ksplit ignored; mode 2: 64 output rows per CTA
+   (max_rows bounds m), each term read coalesced in its own layout (rows
+   across lanes for op(A) = A, k across lanes for op(A) = A^T), K split into
+   ks = min(ksplit, max(1, K / 512)) slices (K summed over the terms): with
+   ks > 1, ws holds ceil(m_cap / 64) x ks_cap slots of 64 x NC doubles (slot
+   (row block, z) at (rb * ks_cap + z) * 64 * NC, NC = 2 for ncmax <= 2 else 4)
+   and cnt one counter per row block; modes 3 / 4: mode 2 specialised to
+   launches whose terms are all op(A) = A / all op(A) = A^T; mode 5: one
+   launch over problems of different K (all op(A) = A^T, one term each):
+   problem i owns work items [item0_i, item0_{i+1}) -- its K slices -- and
+   the grid is ksplit = the total item count; every CTA covers all output
+   rows of its problem: with more than one item, ws holds one slot of
+   m_cap x NC (row-major NC) per item and cnt one counter */
 int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob, const hq_gemm_term* terms,
                    int* rank, int ksplit, int ncmax, int mode, int max_rows, const int* skip);
 int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_piece* pieces,

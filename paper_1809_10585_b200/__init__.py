@@ -8,12 +8,15 @@ matrix with the host containers, then ``hqr(a, eps)`` factors it on the GPU
 from .hodlr import (GENERAL, UNIT_LOWER_TRIANGULAR, UPPER_TRIANGULAR, HodlrMatrix,
                     LowRankBlock, PartitionTree, TruncationControl, build_partition,
                     hodlr_identity, stats, to_dense, validate_structure)
-from .hqr import (HodlrQRFactors, HQREngine, PlanIO, RankCapacityError, engine_for, hqr,
+from .hqr import (HodlrQRFactors, HQREngine, PlanIO, RankCapacityError, clear_engines, engine_for, hqr,
                   hqr_batched)
+from .operators import (HodlrOperator, QROperator, apply_dense, apply_q, apply_q_transpose,
+                        apply_transpose_dense, metrics)
 
 __version__ = "0.1.0"
 
 __all__ = ["GENERAL", "UNIT_LOWER_TRIANGULAR", "UPPER_TRIANGULAR", "HodlrMatrix", "LowRankBlock",
            "PartitionTree", "TruncationControl", "build_partition", "hodlr_identity", "stats",
            "to_dense", "validate_structure", "HodlrQRFactors", "HQREngine", "PlanIO",
-           "RankCapacityError", "engine_for", "hqr", "hqr_batched"]
+           "RankCapacityError", "clear_engines", "engine_for", "hqr", "hqr_batched", "HodlrOperator",
+           "QROperator", "apply_dense", "apply_q", "apply_q_transpose", "apply_transpose_dense", "metrics"]

@@ -22,7 +22,8 @@ GEMM_TERM = np.dtype([("a", P), ("b", P), ("lda", I), ("ldb", I), ("ta", I), ("t
                       ("k", I), ("k_ri", I), ("mask_a", I), ("mask_b", I),
                       ("alpha", np.float64)], align=True)
 GEMM_PROB = np.dtype([("c", P), ("ldc", I), ("m", I), ("m_ri", I), ("n", I), ("n_ri", I),
-                      ("term0", I), ("nterm", I), ("item0", I), ("beta", np.float64)], align=True)
+                      ("term0", I), ("nterm", I), ("item0", I), ("beta", np.float64),
+                      ("ws", P), ("cnt", P)], align=True)
 PIECE = np.dtype([("p", P), ("ld", I), ("cols", I), ("cols_ri", I), ("pad_", I),
                   ("alpha", np.float64)], align=True)
 CONCAT_PROB = np.dtype([("dst", P), ("dst2", P), ("ldd", I), ("ldd2", I), ("rows", I),
@@ -78,6 +79,7 @@ SIGNATURES = {
 }
 
 _LIB = None
+ABI_VERSION = 2   # HQ_ABI_VERSION in include/hodlrqr_b200.h
 
 
 class LibraryError(RuntimeError):
@@ -90,13 +92,13 @@ def load(build_if_missing: bool = True):
     if _LIB is not None:
         return _LIB
     if build_if_missing:
-        try:
-            from . import build
-            if build.stale():
+        from . import build
+        if build.stale():
+            try:
                 build.build()
-        except Exception as exc:  # pragma: no cover - depends on toolchain
-            if not os.path.exists(LIB_PATH):
-                raise LibraryError(f"cannot build {LIB_PATH}: {exc}") from exc
+            except Exception as exc:  # pragma: no cover - depends on toolchain
+                # a stale library may have other descriptor layouts: never load it
+                raise LibraryError(f"{LIB_PATH} is out of date and cannot be rebuilt: {exc}") from exc
     if not os.path.exists(LIB_PATH):
         raise LibraryError(f"{LIB_PATH} missing; run `python -m paper_1809_10585_b200.build`")
     lib = ctypes.CDLL(LIB_PATH)
@@ -104,6 +106,9 @@ def load(build_if_missing: bool = True):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
+    got = lib.hq_abi_version()
+    if got != ABI_VERSION:
+        raise LibraryError(f"{LIB_PATH} has ABI version {got}, this binding expects {ABI_VERSION}; rebuild it")
     _LIB = lib
     return lib
 

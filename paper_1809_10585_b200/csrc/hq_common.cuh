@@ -37,6 +37,26 @@ HQ_DEV double block_sum(double v, double* red) {
   return s;
 }
 
+// block-wide maximum of non-negative values (same contract as block_sum)
+HQ_DEV double block_max_nonneg(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (wid == 0) {
+    s = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s = fmax(s, __shfl_xor_sync(0xffffffffu, s, o));
+    if (lane == 0) red[0] = s;
+  }
+  __syncthreads();
+  s = red[0];
+  return s;
+}
+
 // value of a stored matrix element under a triangular mask
 HQ_DEV double hq_mask(double v, int r, int c, int mask) {
   if (mask == 1) return r <= c ? v : 0.0;              // upper incl. diagonal
@@ -45,6 +65,26 @@ HQ_DEV double hq_mask(double v, int r, int c, int mask) {
 }
 
 static inline int hq_err(cudaError_t e) { return (int)e; }
+
+// Deterministic K-split: every slice of an output block has stored its
+// partial sum into its own workspace slot; the CTA whose arrival completes
+// the block's counter (a device int, zero between uses) returns true, resets
+// the counter, and then sums the slots in slice order 0..ks-1 -- the result
+// is independent of which slice finished last.  Called by every thread.
+HQ_DEV bool hq_split_last(int* counter, int ks) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int old = atomicAdd(counter, 1);
+    s_last = old == ks - 1;
+    if (s_last) atomicExch(counter, 0);
+  }
+  __syncthreads();
+  const bool last = s_last != 0;
+  if (last) __threadfence();
+  return last;
+}
 
 // D (8x8, 2 per lane) += A (8x4, 1 per lane) * B (4x8, 1 per lane): FP64 DMMA.
 // Lane l holds A[l>>2][l&3], B[l&3][l>>2], D[l>>2][2(l&3) + {0,1}].

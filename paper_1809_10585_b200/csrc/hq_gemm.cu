@@ -48,12 +48,16 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
   const int i0 = (tile % ntm) * BM, j0 = (tile / ntm) * BN;
   // per-problem split: at least 8 k-tiles per slice (short-K problems of a
   // split launch keep one slice; the output was pre-zeroed either way)
-  int ks = ksplit;
-  int nkt = 0;
-  for (int ti = 0; ti < P.nterm; ++ti)
-    nkt += (hq_dim(rank, terms[P.term0 + ti].k, terms[P.term0 + ti].k_ri) + BK - 1) / BK;
+  int ks = 1, ks_cap = 1;
   if (ksplit > 1) {
+    int nkt = 0, nkt_cap = 0;
+    for (int ti = 0; ti < P.nterm; ++ti) {
+      const hq_gemm_term& T = terms[P.term0 + ti];
+      nkt += (hq_dim(rank, T.k, T.k_ri) + BK - 1) / BK;
+      nkt_cap += (T.k + BK - 1) / BK;
+    }
     ks = min(ksplit, max(1, nkt / 8));
+    ks_cap = min(ksplit, max(1, nkt_cap / 8));
     if ((int)blockIdx.z >= ks) return;
   }
 
@@ -182,6 +186,31 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
   }
   cp_async_wait<0>();
   // ---- epilogue: lane holds D[gq][2tq + {0,1}] of each m8n8 tile
+  if (ks > 1) {
+    // K-split: partial tile into this slice's slot; the last slice to arrive
+    // sums the slots in slice order (deterministic)
+    double* slot0 = P.ws + (size_t)tile * ks_cap * (BM * BN);
+    double* mine = slot0 + (size_t)blockIdx.z * (BM * BN);
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          mine[(wm * TM + a) * 8 + gq + ((wn * TN + b) * 8 + 2 * tq + h) * BM] = acc[a][b][h];
+    if (!hq_split_last(P.cnt + tile, ks)) return;
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = (wm * TM + a) * 8 + gq + ((wn * TN + b) * 8 + 2 * tq + h) * BM;
+          double v = 0.0;
+          for (int z = 0; z < ks; ++z) v += __ldcg(slot0 + (size_t)z * (BM * BN) + e);
+          acc[a][b][h] = v;
+        }
+  }
 #pragma unroll
   for (int a = 0; a < TM; ++a) {
     const int gi = i0 + (wm * TM + a) * 8 + gq;
@@ -193,8 +222,7 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
         const int gj = j0 + (wn * TN + b) * 8 + 2 * tq + h;
         if (gj >= n) continue;
         double* cp = P.c + gi + (size_t)gj * P.ldc;
-        if (ksplit > 1) atomicAdd(cp, acc[a][b][h]);
-        else *cp = (P.beta == 0.0) ? acc[a][b][h] : fma(P.beta, *cp, acc[a][b][h]);
+        *cp = (P.beta == 0.0) ? acc[a][b][h] : fma(P.beta, *cp, acc[a][b][h]);
       }
     }
   }
@@ -264,12 +292,25 @@ __global__ void __launch_bounds__(NT) gemm_skinny_kernel(const hq_gemm_prob* __r
         for (int w = 0; w < NT / 32; ++w) v += red[w][t];
         const int i = i0 + t / NC, j = j0 + t % NC;
         if (i < m && j < n) {
-          double* cp = P.c + i + (size_t)j * P.ldc;
-          if (ks > 1) atomicAdd(cp, v);
-          else *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
+          if (ks > 1) {
+            P.ws[(size_t)z * P.m * P.n + i + (size_t)j * P.m] = v;
+          } else {
+            double* cp = P.c + i + (size_t)j * P.ldc;
+            *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
+          }
         }
       }
       __syncthreads();
+    }
+  }
+  // K-split: slot z = ws + z * m_cap * n_cap; the last slice sums in order
+  if (ks > 1 && hq_split_last(P.cnt, ks)) {
+    for (int e = t; e < m * n; e += NT) {
+      const int i = e % m, j = e / m;
+      double v = 0.0;
+      for (int zz = 0; zz < ks; ++zz) v += __ldcg(P.ws + (size_t)zz * P.m * P.n + i + (size_t)j * P.m);
+      double* cp = P.c + i + (size_t)j * P.ldc;
+      *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
     }
   }
 }
@@ -357,8 +398,10 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int z = blockIdx.z;
   __shared__ double part[NT / GV_ROWS][GV_ROWS][NC];
-  __shared__ double dotr[GV_ROWS][NC];
-  for (int e = t; e < GV_ROWS * NC; e += NT) dotr[e / NC][e % NC] = 0.0;
+  // A^T-layout sums per k-lane group (a row is shared by up to 8 warps:
+  // separate slots, added in a fixed order -- no shared-memory atomics)
+  __shared__ double dotr[8][GV_ROWS][NC];
+  for (int e = t; e < 8 * GV_ROWS * NC; e += NT) (&dotr[0][0][0])[e] = 0.0;
   __syncthreads();
   const int r = t % GV_ROWS, sl = t / GV_ROWS;
   constexpr int NSL = NT / GV_ROWS;
@@ -366,9 +409,13 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
 #pragma unroll
   for (int j = 0; j < NC; ++j) acc[j] = 0.0;
   // per-problem K split: slices of >= 512 k (the launch's ksplit bounds it)
-  int ktot = 0;
-  for (int ti = 0; ti < P.nterm; ++ti) ktot += hq_dim(rank, terms[P.term0 + ti].k, terms[P.term0 + ti].k_ri);
+  int ktot = 0, ktot_cap = 0;
+  for (int ti = 0; ti < P.nterm; ++ti) {
+    ktot += hq_dim(rank, terms[P.term0 + ti].k, terms[P.term0 + ti].k_ri);
+    ktot_cap += terms[P.term0 + ti].k;
+  }
   const int ks = min(ksplit, max(1, ktot / 512));
+  const int ks_cap = min(ksplit, max(1, ktot_cap / 512));
   if (z >= ks) return;
   // warps per A^T row: spread few rows over all warps
   int wpr = 1;
@@ -477,7 +524,7 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
 #pragma unroll
           for (int j = 0; j < NC; ++j) {
             const double v = warp_sum(d[q][j]);
-            if (lane == 0) atomicAdd(&dotr[r0 + ngrp * (qc + q)][j], T.alpha * v);
+            if (lane == 0) dotr[sub][r0 + ngrp * (qc + q)][j] += T.alpha * v;
           }
         }
       }
@@ -486,15 +533,32 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
 #pragma unroll
   for (int j = 0; j < NC; ++j) part[sl][r][j] = acc[j];
   __syncthreads();
+  // K-split slot of this (row block, slice): 64 x NC doubles
+  double* slot0 = ks > 1 ? P.ws + (size_t)blockIdx.x * ks_cap * (GV_ROWS * NC) : nullptr;
   for (int e = t; e < nr * NC; e += NT) {
     const int rr = e / NC, j = e % NC;
     if (j >= n) continue;
-    double v = dotr[rr][j];
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v += dotr[q][rr][j];
 #pragma unroll
     for (int q = 0; q < NSL; ++q) v += part[q][rr][j];
+    if (ks > 1) {
+      slot0[(size_t)z * (GV_ROWS * NC) + e] = v;
+      continue;
+    }
     double* cp = P.c + (i0 + rr) + (size_t)j * P.ldc;
-    if (ksplit > 1) atomicAdd(cp, v);
-    else *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
+    *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
+  }
+  if (ks > 1 && hq_split_last(P.cnt + blockIdx.x, ks)) {
+    for (int e = t; e < nr * NC; e += NT) {
+      const int rr = e / NC, j = e % NC;
+      if (j >= n) continue;
+      double v = 0.0;
+      for (int zz = 0; zz < ks; ++zz) v += __ldcg(slot0 + (size_t)zz * (GV_ROWS * NC) + e);
+      double* cp = P.c + (i0 + rr) + (size_t)j * P.ldc;
+      *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
+    }
   }
 }
 // Mode 5: the power iteration's V^T X products of every tree level in ONE
@@ -502,8 +566,10 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
 // slices, sized on the host from the static block sizes), so the grid has no
 // empty CTAs; a CTA finds its problem by binary search, then covers all output
 // rows of that problem for its K slice: warp w takes rows w, w+8, ... (RQ at a
-// time, one independent load per row per k step), lanes along k, shuffle
-// reduction, atomic add into C (zeroed by the caller).
+// time, one independent 16-byte load per row per lane and k step), lanes
+// along k, shuffle reduction.  A problem with one item writes C directly; the
+// slices of a split problem write their own workspace slots and the last to
+// arrive sums them in slice order (deterministic).
 template <int NC>
 __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __restrict__ probs,
                                                        const hq_gemm_term* __restrict__ terms,
@@ -523,11 +589,28 @@ __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __res
   const int m = hq_dim(rank, P.m, P.m_ri), n = hq_dim(rank, P.n, P.n_ri);
   if (m <= 0 || n <= 0 || z < 0 || z >= ks) return;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  // destination of this slice: C (one slice) or its slot (row-major NC)
+  double* slot0 = P.ws;
+  double* mine = ks > 1 ? P.ws + (size_t)z * P.m * NC : nullptr;
+  // out(i, j) op= v: first term stores (C: with beta), later terms add; a
+  // barrier separates the terms (row ownership differs between layouts)
+  auto emit = [&](int i, int j, double v, bool first) {
+    if (ks > 1) {
+      double& d = mine[(size_t)i * NC + j];
+      d = first ? v : d + v;
+    } else {
+      double* cp = P.c + i + (size_t)j * P.ldc;
+      *cp = first ? (P.beta == 0.0 ? v : fma(P.beta, *cp, v)) : *cp + v;
+    }
+  };
   for (int ti = 0; ti < P.nterm; ++ti) {
+    const bool first = ti == 0;
+    if (ti > 0) __syncthreads();
     const hq_gemm_term T = terms[P.term0 + ti];
     const int kd = hq_dim(rank, T.k, T.k_ri);
-    const int kb = (int)(((long long)kd * z) / ks), ke = (int)(((long long)kd * (z + 1)) / ks);
-    if (kb >= ke) continue;
+    // slice bounds on multiples of 4 (16-byte aligned vector loads)
+    int kb = (int)(((long long)kd * z) / ks) & ~3, ke = z + 1 == ks ? kd : (int)(((long long)kd * (z + 1)) / ks) & ~3;
+    if (kb > ke) kb = ke;
     const size_t sbk = T.tb == 0 ? 1 : (size_t)T.ldb, sbj = T.tb == 0 ? (size_t)T.ldb : 1;
     if (T.ta == 0) {
       // rows across threads (coalesced columns of A)
@@ -546,11 +629,14 @@ __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __res
         }
 #pragma unroll
         for (int j = 0; j < NC; ++j)
-          if (j < n) atomicAdd(P.c + i + (size_t)j * P.ldc, T.alpha * d[j]);
+          if (j < n) emit(i, j, T.alpha * d[j], first);
       }
       continue;
     }
     const bool plain = T.mask_a == 0 && T.mask_b == 0;
+    // 16-byte loads need even leading dims and 16-byte aligned bases
+    const bool vec = plain && T.tb == 0 && ((T.lda | T.ldb) & 1) == 0 &&
+                     (((uintptr_t)T.a | (uintptr_t)T.b) & 15) == 0;
     for (int r0 = wid; r0 < m; r0 += (NT / 32) * RQ) {
       double d[RQ][NC];
 #pragma unroll
@@ -560,33 +646,34 @@ __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __res
       const double* ap0 = T.a + (size_t)r0 * T.lda;
       const size_t rstep = (size_t)(NT / 32) * T.lda;
       const int nq = min(RQ, (m - 1 - r0) / (NT / 32) + 1);
-      // two k steps per iteration: 2 x (RQ + NC) independent loads in flight
-      int k = kb + lane;
-      for (; k + 32 < ke; k += 64) {
-        double b[2][NC], av[2][RQ];
+      int k = kb;
+      if (vec) {
+        // lane covers k = 2 lane + {0, 1} of every 64-wide step; two steps in
+        // flight: 2 x (RQ + NC) independent 16-byte loads
+        const double2* bcol[NC];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kk = k + 32 * h;
+        for (int j = 0; j < NC; ++j) bcol[j] = reinterpret_cast<const double2*>(T.b + (size_t)(j < n ? j : 0) * T.ldb);
+        for (; k + 128 <= ke; k += 128) {
+          double2 b[2][NC], av[2][RQ];
 #pragma unroll
-          for (int j = 0; j < NC; ++j) {
-            const int jj = j < n ? j : 0;
-            const double v = __ldg(T.b + (size_t)kk * sbk + jj * sbj);
-            b[h][j] = plain ? v : hq_mask(v, T.tb == 0 ? kk : jj, T.tb == 0 ? jj : kk, T.mask_b);
+          for (int h = 0; h < 2; ++h) {
+            const int kk = (k + 64 * h) / 2 + lane;
+#pragma unroll
+            for (int j = 0; j < NC; ++j) b[h][j] = __ldg(bcol[j] + kk);
+#pragma unroll
+            for (int q = 0; q < RQ; ++q)
+              av[h][q] = __ldg(reinterpret_cast<const double2*>(ap0 + (q < nq ? q * rstep : 0)) + kk);
           }
 #pragma unroll
-          for (int q = 0; q < RQ; ++q) {
-            const double v = __ldg(ap0 + (q < nq ? q * rstep : 0) + kk);
-            av[h][q] = plain ? v : hq_mask(v, kk, r0 + (NT / 32) * q, T.mask_a);
-          }
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int q = 0; q < RQ; ++q)
+#pragma unroll
+              for (int j = 0; j < NC; ++j) d[q][j] = fma(av[h][q].y, b[h][j].y, fma(av[h][q].x, b[h][j].x, d[q][j]));
         }
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-          for (int q = 0; q < RQ; ++q)
-#pragma unroll
-            for (int j = 0; j < NC; ++j) d[q][j] = fma(av[h][q], b[h][j], d[q][j]);
       }
-      for (; k < ke; k += 32) {
+      // scalar remainder (and the masked / unaligned case)
+      for (k += lane; k < ke; k += 32) {
         double b[NC];
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
@@ -608,9 +695,18 @@ __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __res
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           const double v = warp_sum(d[q][j]);
-          if (lane == 0 && j < n) atomicAdd(P.c + (r0 + (NT / 32) * q) + (size_t)j * P.ldc, T.alpha * v);
+          if (lane == 0 && j < n) emit(r0 + (NT / 32) * q, j, T.alpha * v, first);
         }
       }
+    }
+  }
+  if (ks > 1 && hq_split_last(P.cnt, ks)) {
+    for (int e = t; e < m * n; e += NT) {
+      const int i = e % m, j = e / m;
+      double v = 0.0;
+      for (int zz = 0; zz < ks; ++zz) v += __ldcg(slot0 + (size_t)zz * P.m * NC + (size_t)i * NC + j);
+      double* cp = P.c + i + (size_t)j * P.ldc;
+      *cp = (P.beta == 0.0) ? v : fma(P.beta, *cp, v);
     }
   }
 }

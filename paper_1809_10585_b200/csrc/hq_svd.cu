@@ -87,11 +87,37 @@ bool g_svd_attr = false;
 }  // namespace
 
 template <int G>
+static cudaLaunchConfig_t cluster_config(cudaStream_t st, int nprob, int smem, cudaLaunchAttribute* at) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nprob * G);
+  cfg.blockDim = dim3(CNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cfg;
+}
+
+// 0: not yet checked, 1: the device can co-schedule a cluster of G CTAs at
+// this shared-memory size, -1: it cannot (e.g. a MIG slice or a GPC with
+// fewer free SMs): such launches run as 8-CTA clusters instead
+template <int G>
+static int& cluster_ok() {
+  static int ok = 0;
+  return ok;
+}
+
+template <int G>
 static int launch_cluster(cudaStream_t st, const hq_svd_prob* probs, int nprob, int* rank,
                           const double* scal) {
   static bool attr = false;
   auto kern = svd_cluster_kernel<G>;
   const int smem = (int)(sizeof(CSmem) > sizeof(SvdSmem) ? sizeof(CSmem) : sizeof(SvdSmem));
+  cudaLaunchAttribute at[1];
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return (int)e;
@@ -101,18 +127,18 @@ static int launch_cluster(cudaStream_t st, const hq_svd_prob* probs, int nprob, 
     }
     attr = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nprob * G);
-  cfg.blockDim = dim3(CNT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = G;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
+  if (G > 8) {
+    int& ok = cluster_ok<G>();
+    if (ok == 0) {
+      cudaLaunchConfig_t probe = cluster_config<G>(st, 1, smem, at);
+      int nclusters = 0;
+      const cudaError_t e = cudaOccupancyMaxActiveClusters(&nclusters, kern, &probe);
+      ok = (e == cudaSuccess && nclusters > 0) ? 1 : -1;
+      if (e != cudaSuccess) (void)cudaGetLastError();
+    }
+    if (ok < 0) return -1;   // caller falls back to a portable cluster size
+  }
+  cudaLaunchConfig_t cfg = cluster_config<G>(st, nprob, smem, at);
   return (int)cudaLaunchKernelEx(&cfg, kern, probs, rank, scal);
 }
 
@@ -125,7 +151,10 @@ extern "C" int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* ra
     if (cluster == 2) return launch_cluster<2>(st, probs, nprob, rank, scal);
     if (cluster <= 4) return launch_cluster<4>(st, probs, nprob, rank, scal);
     if (cluster <= 8) return launch_cluster<8>(st, probs, nprob, rank, scal);
-    return launch_cluster<16>(st, probs, nprob, rank, scal);
+    // 16-CTA clusters only where the device can place them (checked once);
+    // otherwise 8 (a core that outgrows the 8-CTA cluster runs on CTA 0)
+    const int rc = launch_cluster<16>(st, probs, nprob, rank, scal);
+    return rc == -1 ? launch_cluster<8>(st, probs, nprob, rank, scal) : rc;
   }
   if (!g_svd_attr) {
     cudaError_t e = cudaFuncSetAttribute(svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -146,7 +175,7 @@ extern "C" int hq_power_step(void* stream, double* x, double* w, const double* g
   return hq_err(cudaGetLastError());
 }
 
-extern "C" int hq_abi_version(void) { return 1; }
+extern "C" int hq_abi_version(void) { return HQ_ABI_VERSION; }
 
 extern "C" int hq_device_check(void) {
   int dev = 0, major = 0, minor = 0;

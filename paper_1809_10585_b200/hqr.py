@@ -667,15 +667,39 @@ class HQREngine(PlanIO):
         return PlanIO.factors(self, b, hb.numpy(), rk, offs, False, lo)
 
 
-_ENGINES: dict = {}
+from collections import OrderedDict
+
+# engines of recent (tree, batch, eps, mode, capacity) keys, least recently
+# used first.  Each holds a device arena (GBs at n = 16384) and pinned host
+# staging, so only a few are kept: a tolerance sweep or a series of matrix
+# sizes through hqr() evicts (and frees) the oldest instead of growing.
+_ENGINES: "OrderedDict" = OrderedDict()
+MAX_ENGINES = int(os.environ.get("HQB200_MAX_ENGINES", "2"))
+
+
+def clear_engines():
+    """Drop every cached engine (their device arenas are freed)."""
+    _ENGINES.clear()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+    except ImportError:  # pragma: no cover
+        pass
 
 
 def engine_for(tree: PartitionTree, batch=1, eps=1e-10, absolute=False, kcap=512, use_graph=True):
     key = (tuple(tree.leaf_sizes), batch, float(eps), bool(absolute), int(kcap), use_graph)
     eng = _ENGINES.get(key)
-    if eng is None:
-        eng = HQREngine(tree, batch, eps, absolute, kcap, use_graph=use_graph)
-        _ENGINES[key] = eng
+    if eng is not None:
+        _ENGINES.move_to_end(key)
+        return eng
+    while len(_ENGINES) >= max(1, MAX_ENGINES):
+        _ENGINES.popitem(last=False)
+        import torch
+        torch.cuda.empty_cache()
+    eng = HQREngine(tree, batch, eps, absolute, kcap, use_graph=use_graph)
+    _ENGINES[key] = eng
     return eng
 
 

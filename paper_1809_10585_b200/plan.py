@@ -42,8 +42,11 @@ GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
 SKINNY_MAX_COLS = 4  # hq_gemm_skinny: outputs with at most this many columns
 SVD_MAX_N = 1024
 
-R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT, R_SHARED = range(8)
+R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT, R_SHARED, R_WS = range(9)
 LANE_STRIDE = 10   # scratch region of lane l: base + LANE_STRIDE * l (l = 0 main chain)
+GEMM_BK = 16       # k-tile of gemm_kernel (hq_gemm.cu BK)
+GV_ROWS = 64       # output rows per CTA of gemv_kernel (hq_gemm.cu GV_ROWS)
+SPLIT_TARGET = 2 * 2 * 148   # CTAs a K-split launch aims for (148 SMs)
 
 
 class Buf:
@@ -200,14 +203,18 @@ class Builder:
     """Unrolls hqr_rec into batched ops with symbolic addresses."""
 
     def __init__(self, tree: PartitionTree, batch: int, eps: float, absolute: bool,
-                 kcap: int = 512, max_iter: int = 50, tol: float = 1e-3, n_side: int = 3):
+                 kcap: int = 512, max_iter: int = 50, tol: float = 1e-3, n_side: int = 3,
+                 io: bool = True):
+        """io=False: no factorization I/O streams (operator plans build
+        their own, operators.py)."""
         self.tree = Tree(tree)
         self.B = batch
         self.eps, self.absolute = float(eps), bool(absolute)
         self.max_iter, self.tol = max_iter, tol
         self.bumps = {}
-        for r in range(8):
+        for r in range(9):
             self.bump(r)
+        self.n_cnt = 0     # split-K arrival counters (device ints, self-resetting)
         self.lane = 0
         self.n_side = n_side
         self._rr = 0
@@ -223,7 +230,7 @@ class Builder:
         self.PW = self.bumps[R_PERSIST].alloc(2 * n * batch)
         self.PG = self.bumps[R_PERSIST].alloc(4 * batch)
         self.ops = []
-        self.in_items, self.out_items = self._io_items()
+        self.in_items, self.out_items = self._io_items() if io else ([], [])
 
     def _io_items(self):
         """Compact input/output streams: (arena Buf, rows, Dim cols) in a fixed
@@ -309,12 +316,53 @@ class Builder:
         # modes 0/1 remain in the ABI
         tas = {t[2] for p in probs for t in p[5]}
         mode = 3 if tas == {0} else (4 if tas == {1} else 2)
-        if skinny and mode == 0 and ksplit > 1:
-            # a K-slice of >= 8 k per thread amortizes the CTA reduction
-            # (only ever lowered: the caller zeroed C for ksplit > 1)
-            ksplit = max(1, min(ksplit, kmax // 2048))
-        self.op("gemm", probs, dict(tiles=tiles, ksplit=ksplit, skip=skip, skinny=skinny, ncmax=ncmax,
-                                    mode=mode, max_rows=mmax, tile=tile))
+        if ksplit > 1:
+            # split K only as far as the launch needs CTAs: about SPLIT_TARGET
+            # of them (two waves of two per SM); a batch that already fills
+            # the GPU keeps whole K (no partial-sum traffic or workspace)
+            blocks = math.ceil(mmax / GV_ROWS) if skinny else tiles
+            ksplit = max(1, min(ksplit, math.ceil(SPLIT_TARGET / (len(probs) * blocks))))
+        ex = dict(tiles=tiles, ksplit=ksplit, skip=skip, skinny=skinny, ncmax=ncmax,
+                  mode=mode, max_rows=mmax, tile=tile)
+        if ksplit > 1:
+            # deterministic K split: per problem, slots for the partial sums of
+            # every (output block, slice) and one arrival counter per block,
+            # sized from the capacities exactly as the kernels size them
+            slots = []
+            for p in probs:
+                if skinny:
+                    ktot = sum(t[8].cap for t in p[5])
+                    ks = min(ksplit, max(1, ktot // 512))
+                    blocks, per = math.ceil(p[2].cap / GV_ROWS), GV_ROWS * (2 if ncmax <= 2 else 4)
+                else:
+                    nkt = sum(math.ceil(t[8].cap / GEMM_BK) for t in p[5])
+                    ks = min(ksplit, max(1, nkt // 8))
+                    blocks = math.ceil(p[2].cap / tile) * math.ceil(p[3].cap / tile)
+                    per = tile * tile
+                slots.append((blocks, ks, per))
+            self._split_ws(ex, slots)
+        self.op("gemm", probs, ex)
+
+    def take_cnt(self, k):
+        c = self.n_cnt
+        self.n_cnt += int(k)
+        return c
+
+    def _split_ws(self, ex, slots):
+        """slots[i] = (output blocks, slices, doubles per slot) of problem i:
+        workspace in the lane's R_WS region (private to this op; the lane's
+        next op reuses it) and arrival counters, recorded in the op's extra."""
+        wsb = self.lane_bump(R_WS)
+        wsb.reset()
+        ws, cnt = [], []
+        for blocks, ks, per in slots:
+            if ks <= 1:
+                ws.append(None)
+                cnt.append(-1)
+                continue
+            ws.append(wsb.alloc(blocks * ks * per))
+            cnt.append(self.take_cnt(blocks))
+        ex["ws"], ex["cnt"] = ws, cnt
 
     def zero(self, regions):
         if regions:
@@ -343,7 +391,7 @@ class Builder:
         ncap, nris = nc
         ab = self.lane_bump(R_APPLY)
         ab.reset()
-        p1, p2, zeros, kmax = [], [], [], 0
+        p1, p2, kmax = [], [], 0
         tmp = {}
         for b in range(self.B):
             blocks, leafbuf, mask = self._fset(fs, b)
@@ -364,24 +412,25 @@ class Builder:
                         term = (V[u], ncols, 1, 0, X + cols0, ldx, 0, 0, Dim(ncols), 1.0)
                         kmax = max(kmax, ncols)
                     p1.append((buf, kc, Dim(kc, R[u]), Dim(ncap, nris[b]), 0.0, [term]))
-                    zeros.append((buf, kc * ncap))
         if p1 and ncap <= SKINNY_MAX_COLS:
             # streaming V^T X products of every level in one launch (mode 5):
             # each problem gets ceil-ish K/512 work items (<= 32), listed by
-            # prefix sums; outputs are zeroed and accumulated atomically
-            items, tot = [], 0
+            # prefix sums; split problems sum their slices deterministically
+            items, tot, slots = [], 0, []
+            nc = 2 if ncap <= 2 else 4
             for prob in p1:
                 items.append(tot)
-                tot += max(1, min(32, sum(t[8].cap for t in prob[5]) // 512))
-            self.zero(zeros)
-            self.op("gemm", p1, dict(tiles=1, ksplit=tot, skip=skip, skinny=True, ncmax=ncap, mode=5,
-                                     max_rows=max(pr[2].cap for pr in p1), tile=64, items=items))
+                it = max(1, min(32, sum(t[8].cap for t in prob[5]) // 512))
+                tot += it
+                slots.append((1, it, prob[2].cap * nc))
+            ex = dict(tiles=1, ksplit=tot, skip=skip, skinny=True, ncmax=ncap, mode=5,
+                      max_rows=max(pr[2].cap for pr in p1), tile=64, items=items)
+            self._split_ws(ex, slots)
+            self.op("gemm", p1, ex)
         elif p1:
             ksplit = 1
             if kmax >= 1024:
                 ksplit = min(32, kmax // 256)   # per problem the kernel uses <= nktiles/8 slices
-            if ksplit > 1:
-                self.zero(zeros)
             self.gemm(p1, skip=skip, ksplit=ksplit)
         for b in range(self.B):
             blocks, leafbuf, mask = self._fset(fs, b)
@@ -535,8 +584,6 @@ class Builder:
                   [(self.PY + 2 * n * b, n, 1, 0, self.PY + 2 * n * b, n, 0, 0, Dim(n), 1.0)])
                  for b in range(self.B)]
             gs = min(64, max(1, n // 256))
-            if gs > 1:
-                self.zero([(self.PG + 4 * b, 4) for b in range(self.B)])
             self.gemm(g, skip=skip, ksplit=gs)
             self.happly((0, 0), "A", True, ys, ws, (2, [-1] * self.B), skip=skip)
             self.op("power", None, dict(n=n, final=int(it == self.max_iter - 1)))
@@ -692,8 +739,6 @@ class Builder:
         w1 = [self._ph(kc * cap_s) for _ in B]
         cross = [self._sh(m2 * cap_s) for _ in B]
         ks1 = min(32, m1 // 256) if m1 >= 1024 else 1
-        if ks1 > 1:
-            self.zero([(w1[b], kc * cap_s) for b in B])
         self.gemm([(w1[b], kc, Dim(kc, D[b]["rA21"][v]), Dim(cap_s, ks[b]), 0.0,
                     [(D[b]["YV21"][v], m1, 1, 0, sL2[b], m1, 0, 0, Dim(m1), 1.0)]) for b in B],
                   ksplit=ks1)
@@ -738,18 +783,15 @@ class Builder:
             self.trunc(side)
             self.lane = 0
         # slab updates B_R2 -= (Y_B1 S.L) S.R, C2 likewise (hqr.py:158-159)
-        zs, g1, g2, zero = [], [], [], []
+        g1, g2 = [], []
         for b in B:
             for (vc1, yc1, ld, ri, kw), (vc2, yc2, _, _, _) in zip(self.slabs(b, v, c1), self.slabs(b, v, c2)):
                 zb = self._ph(cap_s * kw)
-                zero.append((zb, cap_s * kw))
                 g1.append((zb, cap_s, Dim(cap_s, ks[b]), Dim(kw, ri), 0.0,
                            [(sL2[b], m1, 1, 0, yc1, ld, 0, 0, Dim(m1), 1.0)]))
                 g2.append((vc2, ld, Dim(m2), Dim(kw, ri), 1.0,
                            [(sR[b], m2, 0, 0, zb, cap_s, 0, 0, Dim(cap_s, ks[b]), -1.0)]))
         if g1:
-            if ks1 > 1:
-                self.zero(zero)
             self.gemm(g1, ksplit=ks1)
             self.gemm(g2)
 
@@ -936,7 +978,7 @@ def op_resources(builder, kind, probs, extra):
             slot(extra["skip"])
         for (c, ldc, m, n, beta, terms) in probs:
             wr(c)
-            if beta != 0.0 or extra.get("ksplit", 1) > 1:
+            if beta != 0.0:
                 rd(c)
             slot(m), slot(n)
             for t in terms:
@@ -1066,6 +1108,9 @@ class CompiledPlan:
         self.rank = torch.zeros(max(builder.slots.n, 1), dtype=torch.int32, device=device)
         self.scal = torch.zeros(max(2 * builder.B, 2), dtype=torch.float64, device=device)
         self.totals = torch.zeros(2, dtype=torch.int64, device=device)
+        # split-K arrival counters: zero once, every use leaves them zero
+        self.counters = torch.zeros(max(builder.n_cnt, 1), dtype=torch.int32, device=device)
+        cnt_ptr = self.counters.data_ptr()
         base_ptr = self.arena.data_ptr()
         self.bases = bases
         A = lambda buf: _addr(buf, bases, base_ptr)
@@ -1086,9 +1131,12 @@ class CompiledPlan:
                 nterm = sum(len(p[5]) for p in probs)
                 ta = np.zeros(nterm, _abi.GEMM_TERM)
                 ti = 0
+                wsl = extra.get("ws", [None] * len(probs))
+                cnl = extra.get("cnt", [-1] * len(probs))
                 for i, (c, ldc, m, n, beta, terms) in enumerate(probs):
                     pa[i] = (A(c), ldc, m.cap, m.ri, n.cap, n.ri, ti, len(terms),
-                             extra.get("items", [0] * len(probs))[i], beta)
+                             extra.get("items", [0] * len(probs))[i], beta, A(wsl[i]),
+                             cnt_ptr + 4 * cnl[i] if cnl[i] >= 0 else 0)
                     for (a, lda, tra, ma, bb, ldb, trb, mb, k, alpha) in terms:
                         ta[ti] = (A(a), A(bb), lda, ldb, tra, trb, k.cap, k.ri, ma, mb, alpha)
                         ti += 1

@@ -77,9 +77,9 @@ class Emu:
                     self.masked(self.mat(t["b"], t["ldb"], n, k), t["mask_b"]).T
                 acc += t["alpha"] * (a @ b)
             c = self.mat(p["c"], p["ldc"], m, n)
-            if ex["ksplit"] > 1:
-                c += acc
-            elif p["beta"] == 0.0:
+            # K-split launches sum their slices deterministically: same
+            # contract as an unsplit product (C = beta C + sum of terms)
+            if p["beta"] == 0.0:
                 c[:] = acc
             else:
                 c[:] = p["beta"] * c + acc

@@ -47,7 +47,7 @@ def test_gemm(dev, m, n, k, ta, tb, tile):
     terms = np.zeros(1, _abi.GEMM_TERM)
     terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, 0, 0, -0.5)
     probs = np.zeros(1, _abi.GEMM_PROB)
-    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 1, 0, 2.0)
+    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 1, 0, 2.0, 0, 0)
     dt, dp = put(torch, terms), put(torch, probs)
     tiles = -(-m // tile) * -(-n // tile)
     assert lib.hq_gemm_tiled(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), tiles, 1, tile, None) == 0
@@ -56,31 +56,51 @@ def test_gemm(dev, m, n, k, ta, tb, tile):
     assert np.allclose(back(dC, m, n), ref, atol=1e-12 * max(1, np.abs(ref).max()))
 
 
+def split_buffers(torch, slots, per, counters):
+    """K-split workspace (slots x per doubles, NaN-filled: every slot a
+    launch reads must have been written) and zeroed arrival counters."""
+    ws = torch.full((max(slots * per, 1),), float("nan"), dtype=torch.float64, device="cuda")
+    cnt = torch.zeros(max(counters, 1), dtype=torch.int32, device="cuda")
+    return ws, cnt
+
+
 @pytest.mark.parametrize("tile", [32, 64])
 @pytest.mark.parametrize("m,n,k,ta,tb,ks,masks", [(100, 70, 300, 0, 0, 1, (1, 0)), (33, 90, 257, 1, 0, 3, (2, 0)),
-                                                  (130, 20, 40, 0, 1, 1, (0, 1)), (64, 64, 512, 1, 1, 4, (0, 2))])
+                                                  (130, 20, 40, 0, 1, 1, (0, 1)), (64, 64, 512, 1, 1, 4, (0, 2)),
+                                                  (40, 36, 4000, 1, 0, 16, (0, 0))])
 def test_gemm_terms_masks(dev, m, n, k, ta, tb, ks, masks, tile):
     """hq_gemm_tiled: two terms (k-tiles of both stream through one pipeline),
-    triangular masks, alpha, beta or atomic split-K into a zeroed C."""
+    triangular masks, alpha, beta; K split into slices whose partial sums
+    the last slice adds in slice order (bit-identical reruns, counters left
+    at zero)."""
     torch, lib = dev
     rng = np.random.default_rng(m + 3 * n + 7 * k)
     A = rng.standard_normal((k, m) if ta else (m, k))
     B = rng.standard_normal((n, k) if tb else (k, n))
     A2 = rng.standard_normal((m, 21))
     B2 = rng.standard_normal((21, n))
-    C = rng.standard_normal((m, n)) if ks == 1 else np.zeros((m, n))
+    C = rng.standard_normal((m, n))
     dA, dB, dA2, dB2, dC = (colmajor(torch, x) for x in (A, B, A2, B2, C))
     rank = torch.zeros(4, dtype=torch.int32, device="cuda")
     terms = np.zeros(2, _abi.GEMM_TERM)
     terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, masks[0], masks[1], 0.75)
     terms[1] = (dA2.data_ptr(), dB2.data_ptr(), m, 21, 0, 0, 21, -1, 0, 0, -1.0)
-    probs = np.zeros(1, _abi.GEMM_PROB)
-    beta = 0.5 if ks == 1 else 0.0
-    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta)
-    dt, dp = put(torch, terms), put(torch, probs)
     tiles = -(-m // tile) * -(-n // tile)
-    assert lib.hq_gemm_tiled(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), tiles, ks, tile, None) == 0
-    torch.cuda.synchronize()
+    nkt = -(-k // 16) + -(-21 // 16)
+    ks_cap = min(ks, max(1, nkt // 8))
+    ws, cnt = split_buffers(torch, tiles * ks_cap, tile * tile, tiles)
+    probs = np.zeros(1, _abi.GEMM_PROB)
+    beta = 0.5
+    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta, ws.data_ptr(), cnt.data_ptr())
+    dt, dp = put(torch, terms), put(torch, probs)
+    outs = []
+    for _ in range(2):
+        dC.copy_(colmajor(torch, C))
+        assert lib.hq_gemm_tiled(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), tiles, ks, tile, None) == 0
+        torch.cuda.synchronize()
+        outs.append(back(dC, m, n).copy())
+    assert np.array_equal(outs[0], outs[1])
+    assert int(cnt.abs().sum().item()) == 0
 
     def mask(x, mk):
         if mk == 1:
@@ -93,41 +113,56 @@ def test_gemm_terms_masks(dev, m, n, k, ta, tb, ks, masks, tile):
     opA = (mask(A, masks[0])).T if ta else mask(A, masks[0])
     opB = (mask(B, masks[1])).T if tb else mask(B, masks[1])
     ref = beta * C + 0.75 * (opA @ opB) - A2 @ B2
-    assert np.allclose(back(dC, m, n), ref, atol=1e-11 * max(1, np.abs(ref).max()))
+    assert np.allclose(outs[0], ref, atol=1e-11 * max(1, np.abs(ref).max()))
 
 
 @pytest.mark.parametrize("mode", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("m,n,k,ta,tb,ks,masks", [(16, 2, 8192, 1, 0, 32, (0, 0)), (2, 2, 5000, 1, 0, 19, (0, 0)),
                                                   (256, 2, 256, 0, 0, 1, (1, 0)), (37, 3, 300, 1, 1, 1, (2, 0)),
                                                   (70, 4, 900, 0, 1, 4, (0, 0)), (5, 1, 3, 1, 0, 1, (0, 0)),
-                                                  (600, 2, 40, 1, 0, 1, (0, 2))])
+                                                  (600, 2, 40, 1, 0, 1, (0, 2)), (130, 2, 20000, 1, 0, 16, (0, 0))])
 def test_gemm_skinny(dev, m, n, k, ta, tb, ks, masks, mode):
-    """hq_gemm_skinny: two terms, masks, transposes, beta (ks == 1) or
-    atomic split-K into a zeroed C (ks > 1)."""
+    """hq_gemm_skinny: two terms, masks, transposes, beta; split K with the
+    deterministic slice-order reduction (bit-identical reruns)."""
     torch, lib = dev
     rng = np.random.default_rng(m * 7 + n + k)
     A = rng.standard_normal((k, m) if ta else (m, k))
     B = rng.standard_normal((n, k) if tb else (k, n))
     if (mode == 3 and ta) or (mode == 4 and not ta):
         pytest.skip("layout-specialised mode: every term must match it")
-    ta2 = 1 if mode == 4 else 0   # second term's layout (mode 4: all op(A) = A^T)
+    if mode == 5 and not ta:
+        pytest.skip("mode 5 problems are op(A) = A^T")
+    ta2 = 1 if mode in (4, 5) else 0   # second term's layout (modes 4/5: all op(A) = A^T)
     A2 = rng.standard_normal((m, 5))
     B2 = rng.standard_normal((5, n))
     if mode == 1:
         ks = 1
-    accumulate = ks > 1 or mode == 5   # mode 5 always adds into a zeroed C
-    C = np.zeros((m, n)) if accumulate else rng.standard_normal((m, n))
+    C = rng.standard_normal((m, n))
     dA, dB, dA2, dB2, dC = (colmajor(torch, x) for x in (A, B, A2.T if ta2 else A2, B2, C))
     rank = torch.zeros(4, dtype=torch.int32, device="cuda")
     terms = np.zeros(2, _abi.GEMM_TERM)
     terms[0] = (dA.data_ptr(), dB.data_ptr(), A.shape[0], B.shape[0], ta, tb, k, -1, masks[0], masks[1], 0.75)
     terms[1] = (dA2.data_ptr(), dB2.data_ptr(), 5 if ta2 else m, 5, ta2, 0, 5, -1, 0, 0, -1.0)
+    nc = 2 if n <= 2 else 4
+    if mode == 0:
+        ws, cnt = split_buffers(torch, ks, m * n, 1)
+    elif mode == 5:
+        ws, cnt = split_buffers(torch, ks, m * nc, 1)
+    else:
+        ks_cap = min(ks, max(1, (k + 5) // 512))
+        ws, cnt = split_buffers(torch, -(-m // 64) * ks_cap, 64 * nc, -(-m // 64))
     probs = np.zeros(1, _abi.GEMM_PROB)
-    beta = 0.0 if accumulate else 0.5
-    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta)
+    beta = 0.5
+    probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta, ws.data_ptr(), cnt.data_ptr())
     dt, dp = put(torch, terms), put(torch, probs)
-    assert lib.hq_gemm_skinny(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), ks, n, mode, m, None) == 0
-    torch.cuda.synchronize()
+    outs = []
+    for _ in range(2):
+        dC.copy_(colmajor(torch, C))
+        assert lib.hq_gemm_skinny(None, dp.data_ptr(), 1, dt.data_ptr(), rank.data_ptr(), ks, n, mode, m, None) == 0
+        torch.cuda.synchronize()
+        outs.append(back(dC, m, n).copy())
+    assert np.array_equal(outs[0], outs[1])
+    assert int(cnt.abs().sum().item()) == 0
 
     def mask(x, mk):
         if mk == 1:
@@ -140,7 +175,7 @@ def test_gemm_skinny(dev, m, n, k, ta, tb, ks, masks, mode):
     opA = (mask(A, masks[0])).T if ta else mask(A, masks[0])
     opB = (mask(B, masks[1])).T if tb else mask(B, masks[1])
     ref = beta * C + 0.75 * (opA @ opB) - A2 @ B2
-    assert np.allclose(back(dC, m, n), ref, atol=1e-11 * max(1, np.abs(ref).max()))
+    assert np.allclose(outs[0], ref, atol=1e-11 * max(1, np.abs(ref).max()))
 
 
 @pytest.mark.parametrize("cl", [1, 2, 8])
@@ -191,12 +226,15 @@ def test_qr_and_applyq(dev, m, k, cl):
     assert np.abs(back(dX, m, c) - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
 
 
-@pytest.mark.parametrize("xform,CL", [(0, 1), (1, 1), (1, 2), (1, 4), (1, 8)])
+@pytest.mark.parametrize("xform,CL", [(0, 1), (1, 1), (1, 2), (1, 4), (1, 8), (1, 16)])
 @pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60),
-                                      (200, 190, 120), (256, 256, 200), (130, 128, 128)])
+                                      (200, 190, 120), (256, 256, 200), (130, 128, 128), (448, 448, 300),
+                                      (600, 300, 250), (640, 200, 150)])
 def test_svd_truncation(dev, m, n, keep, xform, CL):
     if xform == 0 and m >= 150:
         pytest.skip("unpreconditioned Jacobi is not used by the plan at this size")
+    if CL == 16 and m < 256:
+        pytest.skip("16-CTA clusters carry only the widest cores")
     # cluster launches pick one SM / the cluster / the global-memory path from
     # the run-time size, so every (size, cluster) combination must be exact
     MM = m
