@@ -10,6 +10,7 @@ from .hodlr import (GENERAL, UNIT_LOWER_TRIANGULAR, UPPER_TRIANGULAR, HodlrMatri
                     hodlr_identity, stats, to_dense, validate_structure)
 from .hqr import (HodlrQRFactors, HQREngine, PlanIO, RankCapacityError, clear_engines, engine_for, hqr,
                   hqr_batched)
+from .construct import compress_block, from_dense
 from .operators import (HodlrOperator, QROperator, apply_dense, apply_q, apply_q_transpose,
                         apply_transpose_dense, metrics)
 
@@ -19,4 +20,5 @@ __all__ = ["GENERAL", "UNIT_LOWER_TRIANGULAR", "UPPER_TRIANGULAR", "HodlrMatrix"
            "PartitionTree", "TruncationControl", "build_partition", "hodlr_identity", "stats",
            "to_dense", "validate_structure", "HodlrQRFactors", "HQREngine", "PlanIO",
            "RankCapacityError", "clear_engines", "engine_for", "hqr", "hqr_batched", "HodlrOperator",
-           "QROperator", "apply_dense", "apply_q", "apply_q_transpose", "apply_transpose_dense", "metrics"]
+           "QROperator", "apply_dense", "apply_q", "apply_q_transpose", "apply_transpose_dense", "metrics",
+           "compress_block", "from_dense"]

@@ -521,7 +521,7 @@ class Builder:
                          [(R2, ld2, 0, 1, R1, ld1, 1, 1, Dim(kcap, kL), 1.0)]))
             qrc.append((C, tauC, tpC, None, k2, 0, Dim(k2, kR), Dim(k1, kL)))
             svd.append((C, Uk, Xw, k2, k1, Dim(k1, kL), Dim(k2, kR), cap, p["rank_ri"],
-                        self.flag_slot, p["eps_slot"], p["eps_scale"], 1))
+                        p.get("flag", self.flag_slot), p["eps_slot"], p["eps_scale"], 1))
             U, ldu = p["U"]
             V, ldv = p["V"]
             if tsL is None:
@@ -1029,6 +1029,9 @@ def op_resources(builder, kind, probs, extra):
                 rd(W_), wr(S_), slot(msr, True)
             else:
                 rd(S_), wr(W_)
+    elif kind == "copy":
+        for (src, dst, rows, cols, lds, ldd, mode) in probs:
+            rd(src), wr(dst), slot(cols)
     elif kind == "pack_copy":
         if extra["which"] == 1:
             rd(Buf(R_IN, 0))
@@ -1194,6 +1197,11 @@ class CompiledPlan:
                 for i, (S_, W_, lds, ldw, ch, rt, k, nc, msr, mode) in enumerate(probs):
                     pa[i] = (A(S_), A(W_), lds, ldw, ch, rt, k.cap, k.ri, nc.cap, nc.ri, msr, mode)
                 self.launch.append(("rowblk", put(pa), None, len(probs), extra))
+            elif kind == "copy":
+                it = np.zeros(len(probs), _abi.COPY_ITEM)
+                for i, (src, dst, rows, cols, lds, ldd, mode) in enumerate(probs):
+                    it[i] = (A(src), A(dst), rows, cols.cap, cols.ri, lds, ldd, mode)
+                self.launch.append(("copy", put(it), None, len(probs), extra))
             elif kind == "pack_copy":
                 it = np.zeros(len(probs), _abi.COPY_ITEM)
                 for i, (buf, rows, cols, *mode) in enumerate(probs):
@@ -1279,6 +1287,8 @@ class CompiledPlan:
                 rc = lib.hq_leaf_scatter(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
             elif kind == "rowblk":
                 rc = lib.hq_rowblocks(stream_handle, dp + o1, cnt, rk, ex["max_chunks"])
+            elif kind == "copy":
+                rc = lib.hq_copy(stream_handle, dp + o1, cnt, rk)
             elif kind == "pack_copy":
                 rc = lib.hq_pack_offsets(stream_handle, dp + o1, cnt, rk, ex["base_ptr"],
                                          self.totals.data_ptr() + 8 * ex["total"], ex["which"])

@@ -289,6 +289,21 @@ class Emu:
             off += rows * cols
         self.plan.totals.numpy()[ex["total"]] = off
 
+    def copy(self, o1, cnt, ex):
+        for it in self.arr(o1, _abi.COPY_ITEM, cnt):
+            cols = self.dim(it["cols"], it["cols_ri"])
+            rows = int(it["rows"])
+            if not rows or not cols:
+                continue
+            v = np.array(self.mat(it["src"], it["lds"], rows, cols))
+            if it["mode"] == 1:
+                v = np.triu(v)
+            elif it["mode"] == 2:
+                v = np.tril(v, -1)
+                k = min(rows, cols)
+                v[np.arange(k), np.arange(k)] = 1.0
+            self.mat(it["dst"], it["ldd"], rows, cols)[:] = v
+
     def run_interleaved(self, seed):
         """Execute the ops in a random order that respects only the plan's
         lanes (program order within a lane) and cross-lane waits -- what the
@@ -337,6 +352,8 @@ class Emu:
                 self.power(ex)
             elif kind == "pack_copy":
                 self.pack_copy(o1, cnt, ex)
+            elif kind == "copy":
+                self.copy(o1, cnt, ex)
             elif kind == "rowblk":
                 self.rowblk(o1, cnt, ex)
             else:
