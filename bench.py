@@ -307,6 +307,7 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1809_10585_b200.gen import CONFIGS
+    from paper_1809_10585_b200.hqr import HQREngine
     from paper_1809_10585_b200.plan import plan_accounting
     cfg = CONFIGS[args.config]
     n = args.n or cfg["n"]

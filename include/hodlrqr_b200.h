@@ -119,7 +119,8 @@ typedef struct hq_applyq_prob {
    Keeps the k' columns with sigma > thr, thr = eps_scale * scal[eps_slot]
    (eps_slot < 0: eps_scale), writes the left singular vectors U_k (m x k',
    sigma descending) and k' into rank[rank_ri]; k' > cap sets rank[flag_ri]
-   and clamps.  work: m*n doubles used when X does not fit shared memory.
+   and clamps.  work: ((m + 1) & ~1) * n doubles (X when it does not fit
+   shared memory; always with hq_svd_block).
    (reference: svd + truncation_rank in core.py:250-253, dense.py:93-99) */
 typedef struct hq_svd_prob {
   double* c;
@@ -181,7 +182,7 @@ typedef struct hq_rowblk_prob {
 /* ---- launchers ---------------------------------------------------------- */
 /* bumped whenever a descriptor layout or a launcher signature changes;
    the Python binding refuses a library with another version */
-#define HQ_ABI_VERSION 2
+#define HQ_ABI_VERSION 3
 int hq_abi_version(void);
 int hq_device_check(void);
 
@@ -230,6 +231,13 @@ int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank, i
    max_m bounds the row count (<= 512) and selects the lane-group width */
 int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal,
            int cluster, int max_m);
+/* the same contract as hq_svd (one CTA per problem) by block one-sided
+   Jacobi: blocks of 8 columns, per tournament round one warp per block pair
+   forms the 16 x 16 Gram on the FP64 tensor pipe, diagonalizes it by
+   two-sided Jacobi and applies the accumulated rotation to the 16 columns on
+   the tensor pipe.  work must hold ((m + 1) & ~1) * min(m, n) doubles
+   (16-byte aligned). */
+int hq_svd_block(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal);
 int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,
                    int* rank, int max_nl);
 int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,

@@ -55,7 +55,7 @@ STRUCT_SIZES = {"hq_rowblk_prob": ROWBLK_PROB, "hq_copy_item": COPY_ITEM, "hq_ge
                 "hq_leaf_prob": LEAF_PROB}
 
 EXPORTS = ("hq_abi_version", "hq_device_check", "hq_gemm", "hq_gemm_tiled", "hq_gemm_skinny", "hq_concat", "hq_qr", "hq_applyq",
-           "hq_svd", "hq_leaf_gather", "hq_leaf_scatter", "hq_zero", "hq_power_step", "hq_copy",
+           "hq_svd", "hq_svd_block", "hq_leaf_gather", "hq_leaf_scatter", "hq_zero", "hq_power_step", "hq_copy",
            "hq_pack_offsets", "hq_rowblocks")
 
 _vp, _i, _d, _i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
@@ -69,6 +69,7 @@ SIGNATURES = {
     "hq_qr": [_vp, _vp, _i, _vp, _i],
     "hq_applyq": [_vp, _vp, _i, _vp, _i],
     "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i],
+    "hq_svd_block": [_vp, _vp, _i, _vp, _vp],
     "hq_leaf_gather": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_leaf_scatter": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_zero": [_vp, _vp, _i, _i64],
@@ -79,7 +80,7 @@ SIGNATURES = {
 }
 
 _LIB = None
-ABI_VERSION = 2   # HQ_ABI_VERSION in include/hodlrqr_b200.h
+ABI_VERSION = 3   # HQ_ABI_VERSION in include/hodlrqr_b200.h
 
 
 class LibraryError(RuntimeError):

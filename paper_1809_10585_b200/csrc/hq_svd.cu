@@ -11,6 +11,7 @@
 
 #include "hq_svd_kernel.cuh"
 #include "hq_svd_cluster.cuh"
+#include "hq_svd_block.cuh"
 
 namespace {
 // One iteration tail of the two-vector power method (dense.py:121-141) for a
@@ -163,6 +164,21 @@ extern "C" int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* ra
     g_svd_attr = true;
   }
   svd_kernel<<<nprob, NT, sizeof(SvdSmem), st>>>(probs, rank, scal);
+  return hq_err(cudaGetLastError());
+}
+
+static bool g_bj_attr = false;
+
+extern "C" int hq_svd_block(void* stream, const hq_svd_prob* probs, int nprob, int* rank,
+                            const double* scal) {
+  if (nprob <= 0) return 0;
+  if (!g_bj_attr) {
+    cudaError_t e = cudaFuncSetAttribute(svd_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(BjSmem));
+    if (e != cudaSuccess) return (int)e;
+    g_bj_attr = true;
+  }
+  svd_block_kernel<<<nprob, BJ_NT, sizeof(BjSmem), (cudaStream_t)stream>>>(probs, rank, scal);
   return hq_err(cudaGetLastError());
 }
 

@@ -506,7 +506,7 @@ class Builder:
             npan = max(1, math.ceil(kcap / NB))
             tpL, tpR = z.alloc(npan * NB * NB), z.alloc(npan * NB * NB)
             C, Uk, Mm = z.alloc(k1 * k2), z.alloc(k1 * cap), z.alloc(kcap * cap)
-            Xw = z.alloc(k1 * min(k1, k2))
+            Xw = z.alloc((k1 + 1) // 2 * 2 * min(k1, k2))
             tauC = z.alloc(min(k1, k2))
             tpC = z.alloc(max(1, math.ceil(min(k1, k2) / NB)) * NB * NB)
             kL, kR = self.slots.take(), self.slots.take()
@@ -870,19 +870,27 @@ def qr_cluster(qr_probs):
     return 4 if n <= 37 else 2
 
 
+SVD_BLOCK_MIN = int(os.environ.get("HQ_SVD_BLOCK_MIN", "48"))   # cores this wide go to block Jacobi
+
+
 def svd_cluster(svd_probs):
-    """Cluster size for a Jacobi launch.  Launches with many problems already
-    fill the GPU one CTA each; few-problem launches get an 8-CTA cluster and
-    the kernel picks one SM, the cluster, or the global-memory path from the
-    run-time core size (capacities overstate it)."""
+    """Kernel for a Jacobi launch.  Cores of at least SVD_BLOCK_MIN columns
+    run the block Jacobi (hq_svd_block: 16-column Grams and updates on the
+    tensor pipe, one CTA per problem); narrower ones the scalar kernel:
+    launches with many problems already fill the GPU one CTA each, few-problem
+    launches get an 8-CTA cluster and the kernel picks one SM, the cluster,
+    or the global-memory path from the run-time core size (capacities
+    overstate it)."""
     mmax = max(p[5].cap for p in svd_probs)
     nmax = max(min(p[5].cap, p[6].cap) for p in svd_probs)
     ld = (mmax + 1) // 2 * 2
+    if nmax >= SVD_BLOCK_MIN:
+        return dict(cluster=1, max_m=mmax, block=True)
     if len(svd_probs) > 18 or mmax > 512:
-        return dict(cluster=1, max_m=mmax)
+        return dict(cluster=1, max_m=mmax, block=False)
     if ld * nmax <= SVD_SMEM_DOUBLES and (nmax + 1) // 2 <= SVD_SINGLE_MAX_PAIRS:
-        return dict(cluster=1, max_m=mmax)
-    return dict(cluster=8, max_m=mmax)
+        return dict(cluster=1, max_m=mmax, block=False)
+    return dict(cluster=8, max_m=mmax, block=False)
 
 
 SVD_C_SMEM_DOUBLES, SVD_C_MAX_BS = 26880, 64   # hq_svd_cluster.cuh C_SMEM_DOUBLES / C_MAX_BS
@@ -933,9 +941,11 @@ def retune_clusters(builder, rk, margin=1.1):
             mm, nn = max(mm, m), max(nn, n)
         m2 = min(int(mm * margin) + 1, p[5].cap) if mm else 0
         n2 = min(int(nn * margin) + 1, m2) if nn else 0
-        G = svd_cluster_runtime(len(probs), m2, n2)
-        if G != extra.get("cluster", 1):
+        block = n2 >= SVD_BLOCK_MIN
+        G = 1 if block else svd_cluster_runtime(len(probs), m2, n2)
+        if G != extra.get("cluster", 1) or block != extra.get("block", False):
             extra["cluster"] = G
+            extra["block"] = block
             changed += 1
     return changed
 
@@ -1278,7 +1288,10 @@ class CompiledPlan:
             elif kind == "qr":
                 rc = lib.hq_qr(stream_handle, dp + o1, cnt, rk, ex.get("cluster", 1))
             elif kind == "svd":
-                rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0))
+                if ex.get("block"):
+                    rc = lib.hq_svd_block(stream_handle, dp + o1, cnt, rk, sc)
+                else:
+                    rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0))
             elif kind == "applyq":
                 rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk, ex.get("max_cols", 0))
             elif kind == "leaf_gather":

@@ -264,3 +264,44 @@ def test_svd_truncation(dev, m, n, keep, xform, CL):
     # projection error of C onto span(U) equals the dropped tail (<= thr)
     err = np.linalg.norm(C - U @ (U.T @ C), 2)
     assert err <= thr * 1.0001 + 1e-12 * np.linalg.norm(C, 2)
+
+
+@pytest.mark.parametrize("xform", [0, 1])
+@pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60),
+                                      (200, 190, 120), (256, 256, 200), (130, 128, 128), (448, 448, 300),
+                                      (600, 300, 250), (640, 200, 150), (97, 33, 30), (17, 17, 1)])
+def test_svd_block_truncation(dev, m, n, keep, xform):
+    """hq_svd_block (block Jacobi on the tensor pipe): same contract as
+    hq_svd -- rank by the threshold, orthonormal U_k spanning the kept
+    singular subspace -- on graded spectra down to 1e-14."""
+    torch, lib = dev
+    rng = np.random.default_rng(m * n + 11)
+    u = np.linalg.qr(rng.standard_normal((m, min(m, n))))[0]
+    v = np.linalg.qr(rng.standard_normal((n, min(m, n))))[0]
+    s = np.logspace(0, -14, min(m, n))
+    C = (u * s) @ v.T
+    thr = float(s[keep]) * 1.000001 if keep < len(s) else 0.0
+    dC = colmajor(torch, np.linalg.qr(C.T)[1] if xform else C)
+    ldc = min(m, n) if xform else m
+    k_cols = min(m, n) if xform else n
+    dW = torch.full((((m + 1) // 2 * 2) * k_cols,), float("nan"), dtype=torch.float64, device="cuda")
+    dU = torch.zeros(m * min(m, n), dtype=torch.float64, device="cuda")
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    scal = torch.zeros(2, dtype=torch.float64, device="cuda")
+    p = np.zeros(1, _abi.SVD_PROB)
+    p[0] = (dC.data_ptr(), dU.data_ptr(), dW.data_ptr(), ldc, m, m, -1, n, -1, min(m, n), 0, 1, -1, thr, xform, 0)
+    dp = put(torch, p)
+    assert lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr()) == 0
+    torch.cuda.synchronize()
+    k = int(rank[0].item())
+    assert int(rank[1].item()) == 0, "capacity flag"
+    assert k == min(keep, len(s))
+    U = back(dU, m, min(m, n))[:, :k]
+    assert np.linalg.norm(U.T @ U - np.eye(k)) <= 1e-12 * max(k, 1)
+    err = np.linalg.norm(C - U @ (U.T @ C), 2)
+    assert err <= thr * 1.0001 + 1e-12 * np.linalg.norm(C, 2)
+    # deterministic: a second launch gives the same U bit for bit
+    U1 = back(dU, m, min(m, n)).copy()
+    assert lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr()) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(back(dU, m, min(m, n)), U1)
