@@ -21,7 +21,10 @@
 // reference: svd + truncation_rank in core.py:250-253, dense.py:82-99
 namespace {
 constexpr int BJ_NT = 512, BJ_NW = BJ_NT / 32;
-constexpr int BJ_INNER = 3;   // inner sweeps per task (stops early once G is diagonal)
+#ifndef HQ_BJ_INNER
+#define HQ_BJ_INNER 1
+#endif
+constexpr int BJ_INNER = HQ_BJ_INNER;   // inner sweeps per task (the classic block method: one)
 
 struct BjWarp {
   double G[16][17];
@@ -59,7 +62,7 @@ __device__ __noinline__ bool bj_task(double* __restrict__ X, int ld, int m, int 
   const double* xb = X + (size_t)(vb ? cb : 0) * ld;
   double aa0 = 0.0, aa1 = 0.0, ab0 = 0.0, ab1 = 0.0, bb0 = 0.0, bb1 = 0.0;
   {
-    constexpr int U = 4;   // row groups of 8 in flight
+    constexpr int U = 8;   // row groups of 8 in flight (16 x 16-byte loads per lane)
     int r0 = 0;
     for (; r0 + 8 * U <= ld; r0 += 8 * U) {
       double2 fa[U], fb[U];
@@ -209,23 +212,33 @@ __device__ __noinline__ bool bj_task(double* __restrict__ X, int ld, int m, int 
   for (int h = 0; h < 2; ++h)
 #pragma unroll
     for (int e = 0; e < 2; ++e) oc[h][e] = gcol(8 * h + 2 * tq + e);
-  for (int r0 = 0; r0 < m; r0 += 8) {
-    const int i = r0 + gq;
-    const bool in = i < m;
-    double av[4];
+  // 4 row tiles per step: their 16 loads per lane are in flight together
+  // (rows are independent, so a step's loads precede its own stores only)
+  constexpr int T4 = 4;
+  for (int r0 = 0; r0 < m; r0 += 8 * T4) {
+    double av[T4][4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) av[s] = (in && ac[s] >= 0) ? X[i + (size_t)ac[s] * ld] : 0.0;
-    double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int u = 0; u < T4; ++u) {
+      const int i = r0 + 8 * u + gq;
+      const bool in = i < m;
 #pragma unroll
-    for (int s = 0; s < 4; ++s)
+      for (int s = 0; s < 4; ++s) av[u][s] = (in && ac[s] >= 0) ? X[i + (size_t)ac[s] * ld] : 0.0;
+    }
 #pragma unroll
-      for (int h = 0; h < 2; ++h) dmma884(d[h][0], d[h][1], av[s], vb_[s][h]);
-    if (in) {
+    for (int u = 0; u < T4; ++u) {
+      const int i = r0 + 8 * u + gq;
+      double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int s = 0; s < 4; ++s)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (oc[h][e] >= 0) X[i + (size_t)oc[h][e] * ld] = d[h][e];
+        for (int h = 0; h < 2; ++h) dmma884(d[h][0], d[h][1], av[u][s], vb_[s][h]);
+      if (i < m) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (oc[h][e] >= 0) X[i + (size_t)oc[h][e] * ld] = d[h][e];
+      }
     }
   }
   __syncwarp();

@@ -123,9 +123,11 @@ class PlanIO:
     item offsets are prefix sums of rows x (capacity or run-time rank)."""
 
     def __init__(self, tree: PartitionTree, batch: int = 1, eps: float = 1e-10,
-                 absolute: bool = False, kcap: int = 512):
+                 absolute: bool = False, kcap: int = 512, builder: Builder = None):
+        """builder: an already built plan of these parameters (e.g. a tracked
+        one for distributed.py); default: build it."""
         self.tree, self.B, self.eps, self.absolute, self.kcap = tree, batch, eps, absolute, kcap
-        self.builder = Builder(tree, batch, eps, absolute, kcap).build()
+        self.builder = builder if builder is not None else Builder(tree, batch, eps, absolute, kcap).build()
         bld = self.builder
         self.inbuf = np.zeros(max(bld.bumps[R_IN].peak, 1))
         self.outbuf = np.zeros(max(bld.bumps[R_OUT].peak, 1))

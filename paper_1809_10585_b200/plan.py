@@ -76,17 +76,30 @@ class Bump:
     def __init__(self, reg):
         self.reg, self.top, self.peak = reg, 0, 0
         self.starts = set()
+        self.live = []     # (start, size) of the allocations since the last reset
+        self.gen = 0       # reset count: instances of different phases differ
 
     def alloc(self, n):
         n = int(max(n, 1))
         b = Buf(self.reg, self.top)
         self.starts.add(self.top)
-        self.top += (n + 7) // 8 * 8
+        size = (n + 7) // 8 * 8
+        self.live.append((self.top, size))
+        self.top += size
         self.peak = max(self.peak, self.top)
         return b
 
     def reset(self):
         self.top = 0
+        self.live = []
+        self.gen += 1
+
+    def instance(self, off):
+        """(start, size, generation) of the live allocation holding off."""
+        import bisect
+        i = bisect.bisect_right(self.live, (off, float("inf"))) - 1
+        s, n = self.live[max(i, 0)]
+        return s, n, self.gen
 
     def finalize(self):
         self.sorted = sorted(self.starts)
@@ -204,9 +217,12 @@ class Builder:
 
     def __init__(self, tree: PartitionTree, batch: int, eps: float, absolute: bool,
                  kcap: int = 512, max_iter: int = 50, tol: float = 1e-3, n_side: int = 3,
-                 io: bool = True):
+                 io: bool = True, track: bool = False):
         """io=False: no factorization I/O streams (operator plans build
-        their own, operators.py)."""
+        their own, operators.py).  track: record per op the allocation
+        instances it reads / writes (multi-GPU partitioning, distributed.py)."""
+        self.track = bool(track)
+        self.cur_level = -1
         self.tree = Tree(tree)
         self.B = batch
         self.eps, self.absolute = float(eps), bool(absolute)
@@ -288,9 +304,21 @@ class Builder:
     def op(self, kind, probs, extra=None):
         extra = dict(extra or {})
         extra["lane"] = self.lane
+        extra["level"] = self.cur_level
         if kind == "qr" and "cluster" not in extra:
             extra["cluster"] = qr_cluster(probs)
+        if self.track:
+            # the live allocation instances this op touches, resolved now
+            # (scratch regions are reused later): the units distributed.py
+            # moves between GPUs
+            extra["_inst"] = op_resources(self, kind, probs, extra, mem=self._inst_key)
         self.ops.append((kind, probs, extra))
+
+    def _inst_key(self, buf):
+        if buf is None:
+            return None
+        s, n, g = self.bumps[buf.reg].instance(buf.off)
+        return ("i", buf.reg, s, n, g)
 
     def gemm(self, probs, skip=None, ksplit=1):
         """probs: list of (c, ldc, Dim m, Dim n, beta, [terms]); term =
@@ -634,6 +662,7 @@ class Builder:
     def leaf_qr(self, v):
         """Compressed leaf column -> block_qr (hqr.py:110-119)."""
         t = self.tree
+        self.cur_level = v[0]
         self.lane = 0
         self.lane_bump(R_PHASE).reset()
         nl = t.size[v]
@@ -660,6 +689,7 @@ class Builder:
         """hqr.py:134-159: S~ (one recompression of the four-term sum), S, the
         R coupling block, and the update of the second block column."""
         t = self.tree
+        self.cur_level = v[0]
         self.lane = 0
         self.lane_bump(R_PHASE).reset()
         c1, c2 = t.children(v)
@@ -800,6 +830,7 @@ class Builder:
         T12 = -T1 T~12 T2.  Runs on a side lane: only later S-phases (through
         T(c1) of an ancestor) and the output read T12."""
         t = self.tree
+        self.cur_level = v[0]
         self.lane = self.side_lane()
         self.lane_bump(R_PHASE).reset()
         c1, c2 = t.children(v)
@@ -956,17 +987,19 @@ def _addr(buf, bases, base_ptr):
     return base_ptr + 8 * (bases[buf.reg] + buf.off)
 
 
-def op_resources(builder, kind, probs, extra):
+def op_resources(builder, kind, probs, extra, mem=None):
     """(reads, writes) of one op: allocations touched ('m', region, start),
     rank-table slots ('r', slot) and the scalar table ('scal',).  The rank
-    capacity-overflow flag is excluded (it is only ever set)."""
+    capacity-overflow flag is excluded (it is only ever set).  mem: optional
+    Buf -> key map (default: the allocation start after finalize())."""
     R, W = set(), set()
     bumps = builder.bumps
 
-    def mem(buf):
-        if buf is None:
-            return None
-        return ("m", buf.reg, bumps[buf.reg].owner(buf.off))
+    if mem is None:
+        def mem(buf):
+            if buf is None:
+                return None
+            return ("m", buf.reg, bumps[buf.reg].owner(buf.off))
 
     def rd(buf):
         k = mem(buf)
@@ -1048,7 +1081,7 @@ def op_resources(builder, kind, probs, extra):
             for (buf, rows, cols, *_) in probs:
                 wr(buf), slot(cols)
         else:
-            W.add(("m", R_OUT, 0)), W.add(("totals",))
+            wr(Buf(R_OUT, 0)), W.add(("totals",))
             for (buf, rows, cols, *_) in probs:
                 rd(buf), slot(cols)
     else:

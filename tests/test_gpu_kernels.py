@@ -274,6 +274,8 @@ def test_svd_block_truncation(dev, m, n, keep, xform):
     """hq_svd_block (block Jacobi on the tensor pipe): same contract as
     hq_svd -- rank by the threshold, orthonormal U_k spanning the kept
     singular subspace -- on graded spectra down to 1e-14."""
+    if xform == 0 and m >= 150:
+        pytest.skip("unpreconditioned cores this large are not issued by the plan")
     torch, lib = dev
     rng = np.random.default_rng(m * n + 11)
     u = np.linalg.qr(rng.standard_normal((m, min(m, n))))[0]
