@@ -901,7 +901,23 @@ def qr_cluster(qr_probs):
     return 4 if n <= 37 else 2
 
 
-SVD_BLOCK_MIN = int(os.environ.get("HQ_SVD_BLOCK_MIN", "48"))   # cores this wide go to block Jacobi
+SVD_BLOCK_MIN = int(os.environ.get("HQ_SVD_BLOCK_MIN", "256"))   # block Jacobi candidates: cores this wide
+
+
+def svd_use_block(nprob, m, n, G=None):
+    """Block Jacobi (hq_svd_block) instead of the scalar kernel: for cores
+    the scalar kernel could only run on one CTA from global memory, and for
+    wide cores whose clusters would take several waves of the 148 SMs
+    (measured, tools/jacobi_ab.py / profiles/r02_jacobi_ab.txt: 56 cores of
+    300 columns 27.6 -> 20.2 ms, 450: 189 -> 61 ms, 560: 1466 -> 128 ms;
+    below ~250 columns the scalar kernel is faster)."""
+    if n <= 0 or m <= 0:
+        return False
+    if G is None:
+        G = svd_cluster_runtime(nprob, m, n)
+    scalar_global = G == 1 and not (_svd_fits(1, m, n) and (n + 1) // 2 <= SVD_SINGLE_MAX_PAIRS) \
+        and not _svd_fits(2, m, n)
+    return scalar_global or (n >= SVD_BLOCK_MIN and nprob * G > 148)
 
 
 def svd_cluster(svd_probs):
@@ -915,7 +931,7 @@ def svd_cluster(svd_probs):
     mmax = max(p[5].cap for p in svd_probs)
     nmax = max(min(p[5].cap, p[6].cap) for p in svd_probs)
     ld = (mmax + 1) // 2 * 2
-    if nmax >= SVD_BLOCK_MIN:
+    if svd_use_block(len(svd_probs), mmax, nmax):
         return dict(cluster=1, max_m=mmax, block=True)
     if len(svd_probs) > 18 or mmax > 512:
         return dict(cluster=1, max_m=mmax, block=False)
@@ -972,8 +988,10 @@ def retune_clusters(builder, rk, margin=1.1):
             mm, nn = max(mm, m), max(nn, n)
         m2 = min(int(mm * margin) + 1, p[5].cap) if mm else 0
         n2 = min(int(nn * margin) + 1, m2) if nn else 0
-        block = n2 >= SVD_BLOCK_MIN
-        G = 1 if block else svd_cluster_runtime(len(probs), m2, n2)
+        G = svd_cluster_runtime(len(probs), m2, n2)
+        block = svd_use_block(len(probs), m2, n2, G)
+        if block:
+            G = 1
         if G != extra.get("cluster", 1) or block != extra.get("block", False):
             extra["cluster"] = G
             extra["block"] = block

@@ -244,7 +244,9 @@ def test_svd_truncation(dev, m, n, keep, xform, CL):
     v = np.linalg.qr(rng.standard_normal((n, min(m, n))))[0]
     s = np.logspace(0, -14, min(m, n))
     C = (u * s) @ v.T
-    thr = float(s[keep]) * 1.000001 if keep < len(s) else 0.0
+    # threshold between sigma_keep-1 and sigma_keep (geometric mid-point: the
+    # smallest kept sigma is ~1e-12 here, known to eps ||C|| absolutely)
+    thr = float(np.sqrt(s[keep - 1] * s[keep])) if keep < len(s) else 0.0
     # xform=1 feeds R of C^T = Q R (the LQ preconditioner); X = R^T
     dC = colmajor(torch, np.linalg.qr(C.T)[1] if xform else C)
     ldc = min(m, n) if xform else m
@@ -282,7 +284,9 @@ def test_svd_block_truncation(dev, m, n, keep, xform):
     v = np.linalg.qr(rng.standard_normal((n, min(m, n))))[0]
     s = np.logspace(0, -14, min(m, n))
     C = (u * s) @ v.T
-    thr = float(s[keep]) * 1.000001 if keep < len(s) else 0.0
+    # threshold between sigma_keep-1 and sigma_keep (geometric mid-point: the
+    # smallest kept sigma is ~1e-12 here, known to eps ||C|| absolutely)
+    thr = float(np.sqrt(s[keep - 1] * s[keep])) if keep < len(s) else 0.0
     dC = colmajor(torch, np.linalg.qr(C.T)[1] if xform else C)
     ldc = min(m, n) if xform else m
     k_cols = min(m, n) if xform else n
