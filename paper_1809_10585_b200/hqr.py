@@ -37,6 +37,38 @@ class HodlrQRFactors:
     r: HodlrMatrix
 
 
+@dataclass
+class StructuredColumn:
+    """Recursion input [a_tilde; b; c] of hqr_rec (reference hqr.py:38-56):
+    an m x m HODLR block, a factorized p x m low-rank block and r2 x m dense
+    coupling rows.  b and c may both be empty."""
+    a_tilde: HodlrMatrix
+    b: LowRankBlock
+    c: np.ndarray
+
+    def __post_init__(self):
+        m = self.a_tilde.n
+        self.c = np.asarray(self.c, dtype=float).reshape(-1, m)
+        if self.b.n_cols != m:
+            raise ValueError("column counts of a_tilde and b must agree")
+
+    @staticmethod
+    def whole_matrix(a: HodlrMatrix) -> "StructuredColumn":
+        return StructuredColumn(a, LowRankBlock.zero(0, a.n), np.zeros((0, a.n)))
+
+
+@dataclass
+class StructuredY:
+    """Mirror of StructuredColumn for the reflector factor Y (hqr.py:59-68)."""
+    y_a: HodlrMatrix
+    y_b: LowRankBlock
+    y_c: np.ndarray
+
+    def to_dense(self) -> np.ndarray:
+        from .hodlr import to_dense as hodlr_to_dense
+        return np.vstack([hodlr_to_dense(self.y_a), self.y_b.to_dense(), self.y_c])
+
+
 def _require_cuda():
     import torch
     if not torch.cuda.is_available():
@@ -159,9 +191,13 @@ class PlanIO:
 
     def _sources(self, b, a):
         """Rank-table entries and the input arrays of matrix b in stream order
-        (leaves, then per internal node a12.L, a12.R^T, a21.L, a21.R^T)."""
+        (leaves, then per internal node a12.L, a12.R^T, a21.L, a21.R^T; for a
+        structured column then B.L, B.R^T and C^T)."""
         bld = self.builder
         t, lay = bld.tree, bld.lay
+        col = a if hasattr(a, "a_tilde") else None
+        if col is not None:
+            a = col.a_tilde
         if tuple(a.leaf_sizes()) != tuple(self.tree.leaf_sizes):
             raise ValueError("matrix does not match the plan's partition tree")
         nodes = self._nodes(a, t)
@@ -175,6 +211,22 @@ class PlanIO:
                     raise RankCapacityError(f"input block rank {blk.rank} exceeds capacity {kc}")
                 self.rk[d[slot][u]] = blk.rank
             srcs += [h.a12.L, h.a12.R.T, h.a21.L, h.a21.R.T]
+        if bld.root_b is not None or bld.root_c:
+            if col is None:
+                raise ValueError("this plan factors structured columns [A; B; C]")
+            if bld.root_b is not None:
+                p_, k_ = bld.root_b
+                if col.b.n_rows != p_ or col.b.rank > k_:
+                    raise ValueError("B does not match the plan's structured column shape")
+                self.rk[d["rBin"]] = col.b.rank
+                srcs += [col.b.L, col.b.R.T]
+            if bld.root_c:
+                if col.c.shape[0] != bld.root_c:
+                    raise ValueError("C does not match the plan's structured column shape")
+                self.rk[d["rC"]] = bld.root_c
+                srcs.append(col.c.T)
+        elif col is not None and (col.b.n_rows or col.c.shape[0]):
+            raise ValueError("this plan factors whole matrices (empty B and C)")
         return srcs
 
     def pack_async(self, mats):
@@ -204,7 +256,8 @@ class PlanIO:
         sc = self.sc
         sc[:] = 0.0
         if self.absolute:
-            sc[1::2] = self.eps
+            # hqr_rec passes its own threshold for the intermediate sums
+            sc[1::2] = self.eps if getattr(self, "eps_abs", None) is None else self.eps_abs
             for b in range(self.B):
                 self.rk[bld.power_done + b] = 1
             self.rk[bld.all_done] = 1
@@ -284,6 +337,14 @@ class PlanIO:
             return HodlrMatrix(a11=h1, a22=h2, a12=a12, a21=zero21, shape_tag=UPPER_TRIANGULAR)
 
         out = HodlrQRFactors(y=build((0, 0), "y"), t=build((0, 0), "t"), r=build((0, 0), "r"))
+        if bld.root_b is not None or bld.root_c:
+            n = t.n
+            if bld.root_b is not None:
+                yb = LowRankBlock(get(d["RB_L"]), get(d["RB_Y"]).T, True)
+            else:
+                yb = LowRankBlock.zero(0, n)
+            yc = get(d["RC_Y"]).T if bld.root_c else np.zeros((0, n))
+            out.y_b, out.y_c = yb, yc
         # `build` is a self-referencing closure (a reference cycle): drop the
         # block views it can reach so only the returned factors hold the memory
         blocks.clear()
@@ -295,13 +356,13 @@ class HQREngine(PlanIO):
 
     def __init__(self, tree: PartitionTree, batch: int = 1, eps: float = 1e-10,
                  absolute: bool = False, kcap: int = 512, device=None, use_graph: bool = True,
-                 stream_out: bool = False):
+                 stream_out: bool = False, builder=None):
         """stream_out: keep the compact output stream in its own region and
         run its compaction outside the graph, so factorize_stream() can copy
         one run's factors to the host while the next run computes (costs the
         output region's memory, which otherwise aliases scratch)."""
         torch = _require_cuda()
-        super().__init__(tree, batch, eps, absolute, kcap)
+        super().__init__(tree, batch, eps, absolute, kcap, builder=builder)
         self.torch = torch
         self.device = torch.device(device if device is not None else "cuda")
         self.stream_out = bool(stream_out)
@@ -717,6 +778,46 @@ def hqr(a: HodlrMatrix, eps: float, n_b: int = 32, absolute: bool = False,
         raise ValueError("n_b must be >= 1")
     eng = engine_for(a.tree(), 1, eps, absolute, kcap)
     return eng.factorize([a])[0]
+
+
+def hqr_rec(col, eps_abs: float, eps_plain: float, n_b: int = 32, kcap: int = 512):
+    """One recursion on a structured block column [A; B; C] on the B200
+    (reference hqr.py:95-194): returns (StructuredY, T, R), Y mirroring the
+    column, T and R upper triangular HODLR of A's partition.  Intermediate
+    sums are truncated at eps_abs, T's coupling blocks at eps_plain.  B and C
+    enter the device plan as the outermost slabs of every compressed column;
+    B is left-orthogonalized on the device (SVD basis: the product Y_b is the
+    reference's, its factors may differ by an orthogonal change of basis)."""
+    if n_b < 1:
+        raise ValueError("n_b must be >= 1")
+    if not hasattr(col, "a_tilde"):
+        raise TypeError("hqr_rec expects a StructuredColumn")
+    a = col.a_tilde
+    b, c = col.b, np.asarray(col.c, dtype=float).reshape(-1, a.n)
+    p = b.n_rows if b.rank > 0 else 0
+    eng = _rec_engine(a.tree(), (p, b.rank) if p else None, c.shape[0], eps_plain, kcap)
+    eng.eps_abs = float(eps_abs)
+    f = eng.factorize([col])[0]
+    yb = f.y_b if p else LowRankBlock(np.zeros((b.n_rows, 0)), np.zeros((0, a.n)), True)
+    y = StructuredY(f.y, yb, getattr(f, "y_c", np.zeros((0, a.n))))
+    return y, f.t, f.r
+
+
+def _rec_engine(tree, root_b, root_c, eps_plain, kcap):
+    key = ("rec", tuple(tree.leaf_sizes), root_b, root_c, float(eps_plain), int(kcap))
+    eng = _ENGINES.get(key)
+    if eng is not None:
+        _ENGINES.move_to_end(key)
+        return eng
+    while len(_ENGINES) >= max(1, MAX_ENGINES):
+        _ENGINES.popitem(last=False)
+    torch = _require_cuda()
+    from .plan import Builder
+    bld = Builder(tree, 1, eps_plain, True, kcap, root_b=root_b, root_c=root_c).build()
+    eng = HQREngine(tree, 1, eps_plain, True, kcap, builder=bld)
+    _ENGINES[key] = eng
+    del torch
+    return eng
 
 
 def hqr_batched(mats, eps: float, absolute: bool = False, kcap: int = 512):

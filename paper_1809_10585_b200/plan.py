@@ -217,12 +217,18 @@ class Builder:
 
     def __init__(self, tree: PartitionTree, batch: int, eps: float, absolute: bool,
                  kcap: int = 512, max_iter: int = 50, tol: float = 1e-3, n_side: int = 3,
-                 io: bool = True, track: bool = False):
+                 io: bool = True, track: bool = False, root_b=None, root_c: int = 0):
         """io=False: no factorization I/O streams (operator plans build
         their own, operators.py).  track: record per op the allocation
-        instances it reads / writes (multi-GPU partitioning, distributed.py)."""
+        instances it reads / writes (multi-GPU partitioning, distributed.py).
+        root_b = (p, k), root_c = r2: the general structured column
+        [A; B; C] of hqr_rec (hqr.py:38-56, 95-194) -- B = L R (p x n, rank
+        <= k) and r2 dense coupling rows C below the HODLR block; they enter
+        as two more slabs of every compressed column, outermost."""
         self.track = bool(track)
         self.cur_level = -1
+        self.root_b = (int(root_b[0]), int(root_b[1])) if root_b is not None and root_b[0] > 0 else None
+        self.root_c = int(root_c)
         self.tree = Tree(tree)
         self.B = batch
         self.eps, self.absolute = float(eps), bool(absolute)
@@ -239,6 +245,20 @@ class Builder:
         self.power_done = self.slots.take(batch)
         self.all_done = self.slots.take(2)
         self.lay = Layout(self.tree, batch, kcap, self.bumps[R_PERSIST], self.slots)
+        if self.root_b is not None or self.root_c:
+            n = self.tree.n
+            P = self.bumps[R_PERSIST]
+            for d in self.lay.m:
+                if self.root_b is not None:
+                    p_, k_ = self.root_b
+                    kb = max(1, min(p_, k_, n))
+                    d["kB"], d["kBin"] = kb, max(1, k_)
+                    d["RB_Lin"], d["RB_Rin"] = P.alloc(p_ * d["kBin"]), P.alloc(n * d["kBin"])
+                    d["RB_L"], d["RB_V"], d["RB_Y"] = P.alloc(p_ * kb), P.alloc(n * kb), P.alloc(n * kb)
+                    d["rBin"], d["rB"] = self.slots.take(), self.slots.take()
+                if self.root_c:
+                    d["RC_V"], d["RC_Y"] = P.alloc(n * self.root_c), P.alloc(n * self.root_c)
+                    d["rC"] = self.slots.take()
         # power buffers: contiguous [X_b], [W_b] with stride 2n, G with stride 4
         n = self.tree.n
         self.PX = self.bumps[R_PERSIST].alloc(2 * n * batch)
@@ -271,6 +291,14 @@ class Builder:
                 outs += [(d["A12U"][u], m1, Dim(kc, d["rA12"][u]), 0), (d["A12V"][u], m2, Dim(kc, d["rA12"][u]), 0),
                          (d["A21U"][u], m2, Dim(kc, d["rA21"][u]), 0), (d["YV21"][u], m1, Dim(kc, d["rA21"][u]), 0),
                          (d["T12U"][u], m1, Dim(kc, d["rT12"][u]), 0), (d["T12V"][u], m2, Dim(kc, d["rT12"][u]), 0)]
+            n = t.n
+            if self.root_b is not None:
+                p_ = self.root_b[0]
+                ins += [(d["RB_Lin"], p_, Dim(d["kBin"], d["rBin"])), (d["RB_Rin"], n, Dim(d["kBin"], d["rBin"]))]
+                outs += [(d["RB_L"], p_, Dim(d["kB"], d["rB"]), 0), (d["RB_Y"], n, Dim(d["kB"], d["rB"]), 0)]
+            if self.root_c:
+                ins += [(d["RC_V"], n, Dim(self.root_c))]
+                outs += [(d["RC_Y"], n, Dim(self.root_c), 0)]
         self.bumps[R_IN].alloc(sum(r * c.cap for _, r, c in ins))
         self.bumps[R_OUT].alloc(sum(r * c.cap for _, r, c, _ in outs))
         return ins, outs
@@ -597,7 +625,20 @@ class Builder:
             o = t.off[sub] - t.off[w]
             out.append((d["A21V"][pw] + o, d["YV21"][pw] + o, t.size[w], d["rA21"][pw],
                         self.lay.kc[pw]))
+        # the structured column's own B and C rows (hqr_rec on [A; B; C]):
+        # outermost, B before C (hqr.py:112, 127)
+        o = t.off[sub]
+        if self.root_b is not None:
+            out.append((d["RB_V"] + o, d["RB_Y"] + o, t.n, d["rB"], d["kB"]))
+        if self.root_c:
+            out.append((d["RC_V"] + o, d["RC_Y"] + o, t.n, d["rC"], self.root_c))
         return out
+
+    def first_col(self, v):
+        """Does v's structured column have its own B block (the slab nearest
+        first in slabs())?  First children: their parent's a21 (hqr.py:127);
+        the root: the column's B (hqr_rec); second children: none (hqr.py:163)."""
+        return (v[0] > 0 and v[1] % 2 == 0) or (v == (0, 0) and self.root_b is not None)
 
     def power_iteration(self, n):
         """||A||_2 by the two-vector power method (dense.py:102-141); start
@@ -622,6 +663,18 @@ class Builder:
         self.op("pack_copy", self.in_items, dict(which=1, base=Buf(R_IN, 0), total=0))
         if not self.absolute:
             self.power_iteration(t.n)
+        # the structured column's B: left-orthogonalized (hqr.py:101; core.py:
+        # 229-236) by a truncation at threshold 0 (SVD basis, same product)
+        if self.root_b is not None:
+            probs = []
+            for b in range(self.B):
+                d = self.lay.m[b]
+                p_ = self.root_b[0]
+                probs.append(dict(m=p_, n=t.n, L=[(d["RB_Lin"], p_, Dim(d["kBin"], d["rBin"]), 1.0)],
+                                  R=[(d["RB_Rin"], t.n, Dim(d["kBin"], d["rBin"]), 1.0)],
+                                  eps_slot=-1, eps_scale=0.0, U=(d["RB_L"], p_), V=(d["RB_V"], t.n),
+                                  cap=d["kB"], rank_ri=d["rB"]))
+            self.trunc(probs)
         # left-orthogonalize the a21 blocks of the leftmost spine: the only B
         # blocks never recompressed by an earlier update (core.py:229-236)
         if t.L > 0:
@@ -712,7 +765,7 @@ class Builder:
         rest = [[], []]
         for b in B:
             sl1, sl2 = self.slabs(b, v, c1), self.slabs(b, v, c2)
-            first = v[0] > 0 and v[1] % 2 == 0
+            first = self.first_col(v)
             own[0].append(sl1[:1] if first else [])
             own[1].append(sl2[:1] if first else [])
             rest[0].append(sl1[1:] if first else sl1)
@@ -842,7 +895,7 @@ class Builder:
         self.happly(c2, "Y", True, [(D[b]["A21U"][v], m2) for b in B], [(tmp3[b], m2) for b in B],
                     (kc, [D[b]["rA21"][v] for b in B]))
         # T~12 = T(T(u1 + u2) + u3) with the plain eps (hqr.py:170-179)
-        first = v[0] > 0 and v[1] % 2 == 0
+        first = self.first_col(v)
         cur_L = [[(D[b]["YV21"][v], m1, Dim(kc, D[b]["rA21"][v]), 1.0)] for b in B]
         cur_R = [[(tmp3[b], m2, Dim(kc, D[b]["rA21"][v]), 1.0)] for b in B]
         sl = [(self.slabs(b, v, c1), self.slabs(b, v, c2)) for b in B]

@@ -17,7 +17,8 @@ for ci in cfgs:
         t = time.perf_counter(); f = hqr(a, c["tol"]); ts.append((time.perf_counter() - t) * 1e3); del f
     eng = engine_for(a.tree(), 1, c["tol"], False, 512)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    eng.snapshot_device_input()
+    eng.pack([a]); eng.upload()
+    eng.snapshot_device_input()   # the run state as uploaded (not a finished run's)
     e0.record(eng.stream)
     for _ in range(3):
         eng.restore_device_input(); eng.execute()
