@@ -223,12 +223,15 @@ def auto_batch(torch, ci, n, tol, local, cap=64, kcap=192, stream_out=True):
     """Matrices per step: as many as fit 85 % of the free HBM (the arena of a
     one-matrix plan scales linearly with the batch), at most `cap`."""
     from paper_1809_10585_b200.gen import gen_config
-    from paper_1809_10585_b200.plan import R_OUT, Builder
+    from paper_1809_10585_b200.plan import LANE_STRIDE, R_OUT, R_WS, Builder
     bld = Builder(gen_config(ci, seed=0, n=n).tree(), 1, tol, False, kcap).build()
-    # the output region aliases scratch unless the engine streams its output
-    per_matrix = 8 * sum(b.peak for r, b in bld.bumps.items() if stream_out or r != R_OUT)
+    # the output region aliases scratch unless the engine streams its output;
+    # the K-split workspaces (R_WS lanes) are sized for a 1-matrix launch's
+    # split factors -- a full batch splits little -- so they are counted once
+    ws = sum(b.peak for r, b in bld.bumps.items() if r % LANE_STRIDE == R_WS)
+    per_matrix = 8 * (sum(b.peak for r, b in bld.bumps.items() if stream_out or r != R_OUT) - ws)
     free, _ = torch.cuda.mem_get_info(local)
-    return max(1, min(cap, int(0.85 * free / per_matrix)))
+    return max(1, min(cap, int((0.85 * free - 8 * ws) / per_matrix)))
 
 
 def build_engine(torch, config, n, batch=None, kcap=None, local=0, ws=1, rank=0):

@@ -13,7 +13,7 @@ B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 kcap = int(sys.argv[4]) if len(sys.argv) > 4 else 512
 c = gen.CONFIGS[ci]
 mats = [gen.gen_config(ci, seed=s, n=n) for s in range(B)]
-eng = HQREngine(mats[0].tree(), B, c["tol"], kcap=kcap, use_graph=False)
+eng = HQREngine(mats[0].tree(), B, c["tol"], kcap=kcap, use_graph=False, stream_out=B > 1)
 eng.factorize(mats)
 eng.pack(mats); eng.upload(); torch.cuda.synchronize()
 torch.cuda.profiler.start()
