@@ -60,22 +60,29 @@ struct QrSmem {
 // Reflector of the column x = [x0; v] (dense.py:45-68) from the sum of
 // squares ss of v (scaled by sc, see below), with the reference's sign
 // convention rho = -sign(x0) ||x||, sign(0) = +1, and gamma = 0 for x = 0.
-// The reference divides by max|x| before the norm; here the column is scaled
-// by an exact power of two sc only when max|x| is outside [2^-480, 2^480]
-// (sc = 1 otherwise, so the common path costs nothing and the scaled path
-// rounds exactly like the unscaled one would without over/underflow).
+// The reference divides by max|x| before the norm.  Here the unscaled sum is
+// used whenever x0^2 + ss lies in [2^-900, 2^900]: then no square overflowed
+// and every square that underflowed is below 2^-112 of the total, so the
+// result equals the scaled one to rounding.  Otherwise (rare: zero or tiny
+// columns, overflow, inf/NaN) the column is rescaled by an exact power of two
+// sc chosen from max|x| and the sum recomputed.
 struct Refl { double gamma, rho, inv; };
+HQ_DEV bool refl_safe(double x0, double ss) {
+  const double tot = fma(x0, x0, ss);
+  return tot >= 0x1p-900 && tot <= 0x1p900;   // false for 0, inf and NaN
+}
 HQ_DEV double refl_scale(double amax) {
   return amax < 0x1p-480 ? 0x1p600 : (amax > 0x1p480 ? 0x1p-600 : 1.0);
 }
-HQ_DEV Refl make_refl(double x0, double ss, double sc) {
+// isc = 1 / sc (exact: sc is a power of two)
+HQ_DEV Refl make_refl(double x0, double ss, double sc, double isc) {
   Refl r{0.0, 0.0, 0.0};
   const double xs = x0 * sc;
   const double nrm = sqrt(fma(xs, xs, ss));
   if (nrm != 0.0) {
     const double sg = x0 < 0.0 ? -1.0 : 1.0;   // sign(0) := +1
     const double u1 = xs + sg * nrm;           // no cancellation
-    r.rho = -sg * nrm / sc;
+    r.rho = -sg * nrm * isc;
     const double iu = 1.0 / u1;
     r.inv = sc * iu;                           // y = v * inv
     r.gamma = 2.0 / (1.0 + ss * iu * iu);
@@ -86,23 +93,28 @@ HQ_DEV Refl make_refl(double x0, double ss, double sc) {
 template <int E>
 __device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int lane, double* ybuf,
                                            double* tau, QrSmem& S) {
-  double ss = 0.0, x0 = 0.0, amax = 0.0;
+  double ss = 0.0, x0 = 0.0;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = lane + 32 * e;
     const double v = c[e];
     if (i > j && i < rows) ss = fma(v, v, ss);
-    if (i >= j && i < rows) amax = fmax(amax, fabs(v));
     if (e == (j >> 5)) x0 = v;
   }
   x0 = __shfl_sync(0xffffffffu, x0, j & 31);
+  ss = warp_sum(ss);
+  double sc = 1.0, isc = 1.0;
+  if (!refl_safe(x0, ss)) {   // warp-uniform, rare: rescale by max|x|
+    double amax = 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {   // the two reductions interleaved
-    ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-  }
-  const double sc = refl_scale(amax);
-  if (sc != 1.0) {   // warp-uniform, rare: recompute the scaled sum of squares
+    for (int e = 0; e < E; ++e) {
+      const int i = lane + 32 * e;
+      if (i >= j && i < rows) amax = fmax(amax, fabs(c[e]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    sc = refl_scale(amax);
+    isc = sc == 1.0 ? 1.0 : (sc > 1.0 ? 0x1p-600 : 0x1p600);
     ss = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -112,7 +124,7 @@ __device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int 
     }
     ss = warp_sum(ss);
   }
-  const Refl R = make_refl(x0, ss, sc);
+  const Refl R = make_refl(x0, ss, sc, isc);
   const double gamma = R.gamma, rho = R.rho, inv = R.inv;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
@@ -225,22 +237,23 @@ __device__ __noinline__ void panel_factor_reg(double* P, int ldp, int rows, int 
 __device__ void panel_factor_block(double* P, int ldp, int rows, int pw, double* tau, QrSmem& S) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   for (int j = 0; j < pw; ++j) {
-    double ss = 0.0, amax = 0.0;
-    for (int i = j + t; i < rows; i += NT) {
-      const double v = P[i + (size_t)j * ldp];
-      if (i > j) ss = fma(v, v, ss);
-      amax = fmax(amax, fabs(v));
-    }
+    double ss = 0.0;
+    for (int i = j + 1 + t; i < rows; i += NT) { const double v = P[i + (size_t)j * ldp]; ss = fma(v, v, ss); }
     ss = block_sum(ss, S.red);
-    amax = block_max_nonneg(amax, S.red);
-    const double sc = refl_scale(amax);
-    if (sc != 1.0) {   // block-uniform, rare
+    const double x0 = P[j + (size_t)j * ldp];
+    double sc = 1.0, isc = 1.0;
+    if (!refl_safe(x0, ss)) {   // block-uniform, rare: rescale by max|x|
+      double amax = 0.0;
+      for (int i = j + t; i < rows; i += NT) amax = fmax(amax, fabs(P[i + (size_t)j * ldp]));
+      amax = block_max_nonneg(amax, S.red);
+      sc = refl_scale(amax);
+      isc = sc == 1.0 ? 1.0 : (sc > 1.0 ? 0x1p-600 : 0x1p600);
       ss = 0.0;
       for (int i = j + 1 + t; i < rows; i += NT) { const double v = P[i + (size_t)j * ldp] * sc; ss = fma(v, v, ss); }
       ss = block_sum(ss, S.red);
     }
     if (t == 0) {
-      const Refl R = make_refl(P[j + (size_t)j * ldp], ss, sc);
+      const Refl R = make_refl(x0, ss, sc, isc);
       P[j + (size_t)j * ldp] = R.rho;
       S.scal[0] = R.gamma; S.scal[1] = R.inv;
       tau[j] = R.gamma;

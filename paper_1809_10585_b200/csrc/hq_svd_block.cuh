@@ -284,7 +284,13 @@ __global__ void __launch_bounds__(BJ_NT, 1) svd_block_kernel(const hq_svd_prob* 
   const double tol = 4.0 * sqrt((double)m) * 2.220446049250313e-16;
   const double tol2 = tol * tol, thr2 = thr * thr, tiny2 = (1e-3 * thr) * (1e-3 * thr);
   const int nb = (n + 7) / 8, nbp = nb + (nb & 1), ntask = nbp / 2;
+#ifdef HQ_DEBUG_SWEEPS
+  int nsw = 0;
+#endif
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
+#ifdef HQ_DEBUG_SWEEPS
+    nsw = sweep + 1;
+#endif
     if (t == 0) S.rotf[(sweep + 1) & 1] = 0;
     for (int r = 0; r < nbp - 1; ++r) {
       for (int k = wid; k < ntask; k += BJ_NW) {
@@ -297,6 +303,9 @@ __global__ void __launch_bounds__(BJ_NT, 1) svd_block_kernel(const hq_svd_prob* 
     }
     if (!S.rotf[sweep & 1]) break;
   }
+#ifdef HQ_DEBUG_SWEEPS
+  if (t == 0 && P.flag_ri >= 0) rank[P.flag_ri + 1] = nsw;
+#endif
   // singular values = exact column norms; U_k sorted by descending sigma
   for (int j = wid; j < n; j += BJ_NW) {
     const double* xj = X + (size_t)j * ld;
