@@ -190,8 +190,9 @@ def run_reference(args):
 
 
 def instrument(eng, torch):
-    """One non-graph pass with CUDA events around every launch: per-kind
-    device time (for the roofline of the dominant kernel)."""
+    """One non-graph pass with CUDA events around every launch: device time
+    per kernel class (plan.kind_key) for the rooflines."""
+    from paper_1809_10585_b200.plan import kind_key
     plan = eng.plan
     lib = __import__("paper_1809_10585_b200._abi", fromlist=["load"]).load()
     s = eng.stream
@@ -201,22 +202,32 @@ def instrument(eng, torch):
     s.synchronize()
     evs = []
     orig = plan.launch
+    bld = eng.builder
+    converged = False
+    skipped = set()     # gated launches that were no-ops (power iteration converged)
     with torch.cuda.stream(s):
         for i, rec in enumerate(orig):
+            if converged and rec[4].get("skip") is not None:
+                skipped.add(i)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             plan.launch = [rec]
             plan.run(s.cuda_stream)
             e1.record(s)
-            evs.append((rec[0], e0, e1))
+            evs.append((i, kind_key(rec[0], rec[4]), e0, e1))
+            if rec[0] == "power" and not converged:
+                s.synchronize()
+                converged = bool(plan.rank[bld.all_done].item())
     plan.launch = orig
     s.synchronize()
-    for kind, e0, e1 in evs:
+    for i, kind, e0, e1 in evs:
+        if i in skipped:
+            continue
         d = per.setdefault(kind, [0.0, 0])
         d[0] += e0.elapsed_time(e1)
         d[1] += 1
     del lib
-    return per
+    return per, skipped
 
 
 def auto_batch(torch, ci, n, tol, local, cap=64, kcap=192, stream_out=True):
@@ -469,7 +480,8 @@ def main():
         line["latency_ms_single_matrix_api"] = min(ts)
         clear_engines()
     if not args.no_instrument and rank == 0:
-        per = instrument(eng, torch)
+        per, skipped = instrument(eng, torch)
+        acc = plan_accounting(eng.builder, rk, skipped)
         tot = sum(v[0] for v in per.values())
         kinds = {k: {"ms": v[0], "launches": v[1], "share": v[0] / tot,
                      "gflop": acc.get(k, {}).get("flops", 0.0) / 1e9,
@@ -492,6 +504,27 @@ def main():
                             "flops_per_launch": acc[top]["flops"] / max(acc[top]["launches"], 1),
                             "avg_launch_ms": per[top][0] / per[top][1], "share_of_step": kinds[top]["share"]}
         line["kernel_time_by_kind"] = kinds
+        # every kernel class against its own roof: HBM bytes per launch for the
+        # streaming / data-movement kernels, FP64 DMMA for the rest
+        hbm = 6538.0
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                hbm = float(json.load(fh).get("hbm_gbs", hbm))
+        except (OSError, ValueError):
+            pass
+        rbk = {}
+        for k, v in per.items():
+            a = acc.get(k, {})
+            sec = v[0] / 1e3
+            if k in ("gemv", "concat", "pack_copy", "leaf_gather", "leaf_scatter"):
+                gbs = a.get("bytes", 0.0) / max(sec, 1e-12) / 1e9
+                rbk[k] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                          "bytes_per_launch": a.get("bytes", 0.0) / max(v[1], 1)}
+            elif a.get("flops", 0.0) > 0:
+                tf = a["flops"] / max(sec, 1e-12) / 1e12
+                rbk[k] = {"bound": "tensor", "achieved": tf, "peak": peak_fp64 / 1e12, "unit": "TFLOP/s",
+                          "frac": tf / (peak_fp64 / 1e12), "flops_per_launch": a["flops"] / max(v[1], 1)}
+        line["roofline_by_kind"] = rbk
     if rank == 0 and not args.no_cpu_baseline and ws == 1:
         v_cpu, procs, cnt = cpu_throughput(args.config, n, rounds=1)
         line["cpu_baseline"] = {"value": v_cpu, "unit": UNIT, "cores": procs, "kind": "port",

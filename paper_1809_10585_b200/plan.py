@@ -1474,13 +1474,42 @@ def op_bytes(kind, probs, rk):
     return by
 
 
-def plan_accounting(builder, rk):
-    """Per-op-kind launches / flops / bytes of a finished run."""
+def kind_key(kind, extra):
+    """Kernel class of an op for accounting: the streaming skinny products
+    (HBM-bound GEMVs) apart from the DMMA GEMMs, the block Jacobi apart from
+    the scalar one."""
+    if kind == "gemm" and extra.get("skinny"):
+        return "gemv"
+    if kind == "svd" and extra.get("block"):
+        return "svd_block"
+    return kind
+
+
+def plan_accounting(builder, rk, skipped=None):
+    """Per-kernel-class launches / flops / bytes of a finished run.
+    skipped: indices of the ops that were no-ops in that run (the power
+    iteration's gated launches after convergence); None: count no gated op."""
     acc = {}
-    for kind, probs, extra in builder.ops:
-        a = acc.setdefault(kind, {"launches": 0, "flops": 0.0, "bytes": 0.0})
+    for i, (kind, probs, extra) in enumerate(builder.ops):
+        a = acc.setdefault(kind_key(kind, extra), {"launches": 0, "flops": 0.0, "bytes": 0.0})
         a["launches"] += 1
-        if probs is not None and not (kind == "gemm" and extra.get("skip") is not None):
-            a["flops"] += op_flops(kind, probs, rk)
-            a["bytes"] += op_bytes(kind, probs, rk)
+        gated = extra.get("skip") is not None
+        if probs is None or (gated and (skipped is None or i in skipped)):
+            continue
+        a["flops"] += op_flops(kind, probs, rk)
+        a["bytes"] += op_bytes(kind, probs, rk) if kind != "gemm" or not extra.get("skinny") \
+            else gemv_bytes(probs, rk)
     return acc
+
+
+def gemv_bytes(probs, rk):
+    """Compulsory bytes of a streaming skinny product: every term's A read
+    once, B (k x n, tiny) and C (m x n) once."""
+    by = 0.0
+    for (c, ldc, m, n, beta, terms) in probs:
+        mm, nn = _dv(m, rk), _dv(n, rk)
+        for t in terms:
+            k = _dv(t[8], rk)
+            by += 8.0 * (mm * k + k * nn)
+        by += 8.0 * mm * nn * (2 if beta != 0.0 else 1)
+    return by
