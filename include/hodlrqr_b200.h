@@ -182,7 +182,7 @@ typedef struct hq_rowblk_prob {
 /* ---- launchers ---------------------------------------------------------- */
 /* bumped whenever a descriptor layout or a launcher signature changes;
    the Python binding refuses a library with another version */
-#define HQ_ABI_VERSION 3
+#define HQ_ABI_VERSION 4
 int hq_abi_version(void);
 int hq_device_check(void);
 
@@ -236,8 +236,11 @@ int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const d
    forms the 16 x 16 Gram on the FP64 tensor pipe, diagonalizes it by
    two-sided Jacobi and applies the accumulated rotation to the 16 columns on
    the tensor pipe.  work must hold ((m + 1) & ~1) * min(m, n) doubles
-   (16-byte aligned). */
-int hq_svd_block(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal);
+   (16-byte aligned).  cluster = 2, 4 or 8: each problem on a cluster of that
+   many CTAs (the tasks of a round spread over all its warps, one cluster
+   barrier per round); 1: one CTA per problem. */
+int hq_svd_block(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal,
+                 int cluster);
 int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,
                    int* rank, int max_nl);
 int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,

@@ -69,7 +69,7 @@ SIGNATURES = {
     "hq_qr": [_vp, _vp, _i, _vp, _i],
     "hq_applyq": [_vp, _vp, _i, _vp, _i],
     "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i],
-    "hq_svd_block": [_vp, _vp, _i, _vp, _vp],
+    "hq_svd_block": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_leaf_gather": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_leaf_scatter": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_zero": [_vp, _vp, _i, _i64],
@@ -80,7 +80,7 @@ SIGNATURES = {
 }
 
 _LIB = None
-ABI_VERSION = 3   # HQ_ABI_VERSION in include/hodlrqr_b200.h
+ABI_VERSION = 4   # HQ_ABI_VERSION in include/hodlrqr_b200.h
 
 
 class LibraryError(RuntimeError):

@@ -167,19 +167,42 @@ extern "C" int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* ra
   return hq_err(cudaGetLastError());
 }
 
-static bool g_bj_attr = false;
+template <int G>
+static int launch_block(cudaStream_t st, const hq_svd_prob* probs, int nprob, int* rank, const double* scal) {
+  static bool attr = false;
+  auto kern = svd_block_kernel<G>;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BjSmem));
+    if (e != cudaSuccess) return (int)e;
+    attr = true;
+  }
+  if (G == 1) {
+    kern<<<nprob, BJ_NT, sizeof(BjSmem), st>>>(probs, rank, scal);
+    return hq_err(cudaGetLastError());
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nprob * G);
+  cfg.blockDim = dim3(BJ_NT);
+  cfg.dynamicSmemBytes = sizeof(BjSmem);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, kern, probs, rank, scal);
+}
 
 extern "C" int hq_svd_block(void* stream, const hq_svd_prob* probs, int nprob, int* rank,
-                            const double* scal) {
+                            const double* scal, int cluster) {
   if (nprob <= 0) return 0;
-  if (!g_bj_attr) {
-    cudaError_t e = cudaFuncSetAttribute(svd_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(BjSmem));
-    if (e != cudaSuccess) return (int)e;
-    g_bj_attr = true;
-  }
-  svd_block_kernel<<<nprob, BJ_NT, sizeof(BjSmem), (cudaStream_t)stream>>>(probs, rank, scal);
-  return hq_err(cudaGetLastError());
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cluster >= 8) return launch_block<8>(st, probs, nprob, rank, scal);
+  if (cluster >= 4) return launch_block<4>(st, probs, nprob, rank, scal);
+  if (cluster >= 2) return launch_block<2>(st, probs, nprob, rank, scal);
+  return launch_block<1>(st, probs, nprob, rank, scal);
 }
 
 extern "C" int hq_power_step(void* stream, double* x, double* w, const double* g, int n,

@@ -69,8 +69,8 @@ __device__ __noinline__ bool bj_task(double* __restrict__ X, int ld, int m, int 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int rr = r0 + 8 * u + 2 * tq;
-        fa[u] = va ? *reinterpret_cast<const double2*>(xa + rr) : make_double2(0.0, 0.0);
-        fb[u] = vb ? *reinterpret_cast<const double2*>(xb + rr) : make_double2(0.0, 0.0);
+        fa[u] = va ? __ldcg(reinterpret_cast<const double2*>(xa + rr)) : make_double2(0.0, 0.0);
+        fb[u] = vb ? __ldcg(reinterpret_cast<const double2*>(xb + rr)) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -85,8 +85,8 @@ __device__ __noinline__ bool bj_task(double* __restrict__ X, int ld, int m, int 
     for (; r0 < ld; r0 += 8) {
       const int rr = r0 + 2 * tq;
       const bool in = rr < ld;   // ld even: rr + 1 < ld too
-      const double2 fa = (va && in) ? *reinterpret_cast<const double2*>(xa + rr) : make_double2(0.0, 0.0);
-      const double2 fb = (vb && in) ? *reinterpret_cast<const double2*>(xb + rr) : make_double2(0.0, 0.0);
+      const double2 fa = (va && in) ? __ldcg(reinterpret_cast<const double2*>(xa + rr)) : make_double2(0.0, 0.0);
+      const double2 fb = (vb && in) ? __ldcg(reinterpret_cast<const double2*>(xb + rr)) : make_double2(0.0, 0.0);
       dmma884(aa0, aa1, fa.x, fa.x);
       dmma884(ab0, ab1, fa.x, fb.x);
       dmma884(bb0, bb1, fb.x, fb.x);
@@ -222,7 +222,7 @@ __device__ __noinline__ bool bj_task(double* __restrict__ X, int ld, int m, int 
       const int i = r0 + 8 * u + gq;
       const bool in = i < m;
 #pragma unroll
-      for (int s = 0; s < 4; ++s) av[u][s] = (in && ac[s] >= 0) ? X[i + (size_t)ac[s] * ld] : 0.0;
+      for (int s = 0; s < 4; ++s) av[u][s] = (in && ac[s] >= 0) ? __ldcg(X + i + (size_t)ac[s] * ld) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < T4; ++u) {
@@ -245,42 +245,48 @@ __device__ __noinline__ bool bj_task(double* __restrict__ X, int ld, int m, int 
   return sig;
 }
 
-__global__ void __launch_bounds__(BJ_NT, 1) svd_block_kernel(const hq_svd_prob* __restrict__ probs,
-                                                            int* __restrict__ rank,
-                                                            const double* __restrict__ scal) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  BjSmem& S = *reinterpret_cast<BjSmem*>(smem_raw);
-  const hq_svd_prob P = probs[blockIdx.x];
+// One problem on G CTAs (G = 1: plain launch; G > 1: a thread-block cluster).
+// X lives in global memory (L2; loads bypass L1, __ldcg), so the CTAs of a
+// cluster share it without DSMEM: the tasks of a round are spread over all
+// G x 16 warps and the round ends with one cluster barrier (release /
+// acquire at cluster scope orders the column updates).  Only the sweep's
+// convergence flags travel through distributed shared memory.
+template <int G>
+__device__ __forceinline__ void bj_sync() {
+  if constexpr (G == 1) __syncthreads();
+  else cg::this_cluster().sync();
+}
+
+template <int G>
+__device__ void svd_block_body(const hq_svd_prob& Pin, int* __restrict__ rank, const double* __restrict__ scal,
+                               BjSmem& S) {
+  const hq_svd_prob P = Pin;
+  const int cr = G > 1 ? (int)cg::this_cluster().block_rank() : 0;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int gw = cr * BJ_NW + wid;           // warp index over the cluster
   const int m = hq_dim(rank, P.m, P.m_ri);
   int n = hq_dim(rank, P.n, P.n_ri);
   if (P.xform) n = min(n, m);
   const double thr = P.eps_scale * (P.eps_slot >= 0 ? scal[P.eps_slot] : 1.0);
-  if (t == 0 && P.flag_ri >= 0 && (n > MAX_N || (P.n >= MAX_N && P.n_ri >= 0 && rank[P.n_ri] > P.n)))
+  if (cr == 0 && t == 0 && P.flag_ri >= 0 && (n > MAX_N || (P.n >= MAX_N && P.n_ri >= 0 && rank[P.n_ri] > P.n)))
     rank[P.flag_ri] = 1;
   n = min(n, MAX_N);
   if (m <= 0 || n <= 0) {
-    if (t == 0) rank[P.rank_ri] = 0;
-    return;
+    if (cr == 0 && t == 0) rank[P.rank_ri] = 0;
+    return;   // uniform over the cluster: no CTA waits at a barrier
   }
   // X in the work buffer, even leading dimension (16-byte aligned columns),
   // rows m..ld-1 zero
   const int ld = (m + 1) & ~1;
   double* X = P.work;
-  if (P.xform) {
-    // X[i][j] = R[j][i] (j <= i), R stored in c with leading dim ldc
-    for (int e = t; e < ld * n; e += BJ_NT) {
-      const int i = e % ld, j = e / ld;
-      X[e] = (i < m && j <= i) ? P.c[j + (size_t)i * P.ldc] : 0.0;
-    }
-  } else {
-    for (int e = t; e < ld * n; e += BJ_NT) {
-      const int i = e % ld, j = e / ld;
-      X[e] = i < m ? P.c[i + (size_t)j * P.ldc] : 0.0;
-    }
+  for (int e = cr * BJ_NT + t; e < ld * n; e += G * BJ_NT) {
+    const int i = e % ld, j = e / ld;
+    // xform: X[i][j] = R[j][i] (j <= i), R stored in c with leading dim ldc
+    X[e] = P.xform ? ((i < m && j <= i) ? P.c[j + (size_t)i * P.ldc] : 0.0)
+                   : (i < m ? P.c[i + (size_t)j * P.ldc] : 0.0);
   }
   if (t < 2) S.rotf[t] = 0;
-  __syncthreads();
+  bj_sync<G>();
   const double tol = 4.0 * sqrt((double)m) * 2.220446049250313e-16;
   const double tol2 = tol * tol, thr2 = thr * thr, tiny2 = (1e-3 * thr) * (1e-3 * thr);
   const int nb = (n + 7) / 8, nbp = nb + (nb & 1), ntask = nbp / 2;
@@ -293,24 +299,35 @@ __global__ void __launch_bounds__(BJ_NT, 1) svd_block_kernel(const hq_svd_prob* 
 #endif
     if (t == 0) S.rotf[(sweep + 1) & 1] = 0;
     for (int r = 0; r < nbp - 1; ++r) {
-      for (int k = wid; k < ntask; k += BJ_NW) {
+      for (int k = gw; k < ntask; k += G * BJ_NW) {
         int I, J;
         circle_pair(r, k, nbp, I, J);
         if (I >= nb) continue;   // both blocks are padding
         if (bj_task(X, ld, m, n, I, J, tol2, tiny2, thr2, S.w[wid]) && lane == 0) S.rotf[sweep & 1] = 1;
       }
-      __syncthreads();
+      bj_sync<G>();
     }
-    if (!S.rotf[sweep & 1]) break;
+    int any = S.rotf[sweep & 1];
+    if constexpr (G > 1) {
+      cg::cluster_group cl = cg::this_cluster();
+#pragma unroll
+      for (int c = 0; c < G; ++c) any |= *cl.map_shared_rank(&S.rotf[sweep & 1], c);
+    }
+    if (!any) break;
   }
 #ifdef HQ_DEBUG_SWEEPS
-  if (t == 0 && P.flag_ri >= 0) rank[P.flag_ri + 1] = nsw;
+  if (cr == 0 && t == 0 && P.flag_ri >= 0) rank[P.flag_ri + 1] = nsw;
 #endif
-  // singular values = exact column norms; U_k sorted by descending sigma
+  // singular values = exact column norms (every CTA computes all of them);
+  // U_k sorted by descending sigma, each kept column written by one warp of
+  // the cluster
   for (int j = wid; j < n; j += BJ_NW) {
     const double* xj = X + (size_t)j * ld;
     double v = 0.0;
-    for (int i = lane; i < m; i += 32) v = fma(xj[i], xj[i], v);
+    for (int i = lane; i < m; i += 32) {
+      const double x = __ldcg(xj + i);
+      v = fma(x, x, v);
+    }
     v = sqrt(warp_sum(v));
     if (lane == 0) S.nrm[j] = v;
   }
@@ -319,6 +336,8 @@ __global__ void __launch_bounds__(BJ_NT, 1) svd_block_kernel(const hq_svd_prob* 
   for (int j = wid; j < n; j += BJ_NW) {
     const double sj = S.nrm[j];
     if (!(sj > thr)) continue;
+    if (lane == 0) atomicAdd(&S.cnt, 1);
+    if (j % G != cr) continue;
     int pos = 0;
     for (int o = lane; o < n; o += 32) {
       const double so = S.nrm[o];
@@ -326,18 +345,27 @@ __global__ void __launch_bounds__(BJ_NT, 1) svd_block_kernel(const hq_svd_prob* 
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) pos += __shfl_xor_sync(0xffffffffu, pos, off);
-    if (lane == 0) atomicAdd(&S.cnt, 1);
     if (pos < P.cap) {
       const double inv = 1.0 / sj;
       const double* xj = X + (size_t)j * ld;
-      for (int i = lane; i < m; i += 32) P.u[i + (size_t)pos * P.ldu] = xj[i] * inv;
+      for (int i = lane; i < m; i += 32) P.u[i + (size_t)pos * P.ldu] = __ldcg(xj + i) * inv;
     }
   }
   __syncthreads();
-  if (t == 0) {
+  if (cr == 0 && t == 0) {
     int kk = S.cnt;
     if (kk > P.cap) { if (P.flag_ri >= 0) rank[P.flag_ri] = 1; kk = P.cap; }
     rank[P.rank_ri] = kk;
   }
+  // no CTA leaves while another may still read its flags
+  if constexpr (G > 1) cg::this_cluster().sync();
+}
+
+template <int G>
+__global__ void __launch_bounds__(BJ_NT, 1) svd_block_kernel(const hq_svd_prob* __restrict__ probs,
+                                                            int* __restrict__ rank,
+                                                            const double* __restrict__ scal) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  svd_block_body<G>(probs[blockIdx.x / G], rank, scal, *reinterpret_cast<BjSmem*>(smem_raw));
 }
 }  // namespace

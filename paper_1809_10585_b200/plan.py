@@ -973,6 +973,18 @@ def svd_use_block(nprob, m, n, G=None):
     return scalar_global or (n >= SVD_BLOCK_MIN and nprob * G > 148)
 
 
+def svd_block_cluster(nprob, n, sms=148):
+    """CTAs per problem of a block-Jacobi launch: enough warps (16 per CTA)
+    for one pass over a round's ceil(n/16) block pairs, a power of two <= 8,
+    as long as the launch still fits the SMs."""
+    ntask = -(-(-(-n // 8)) // 2)
+    need = max(1, -(-ntask // 16))
+    G = 1
+    while G < need and G < 8 and nprob * 2 * G <= sms:
+        G *= 2
+    return G
+
+
 def svd_cluster(svd_probs):
     """Kernel for a Jacobi launch.  Cores of at least SVD_BLOCK_MIN columns
     run the block Jacobi (hq_svd_block: 16-column Grams and updates on the
@@ -985,7 +997,7 @@ def svd_cluster(svd_probs):
     nmax = max(min(p[5].cap, p[6].cap) for p in svd_probs)
     ld = (mmax + 1) // 2 * 2
     if svd_use_block(len(svd_probs), mmax, nmax):
-        return dict(cluster=1, max_m=mmax, block=True)
+        return dict(cluster=1, max_m=mmax, block=True, bcluster=svd_block_cluster(len(svd_probs), nmax))
     if len(svd_probs) > 18 or mmax > 512:
         return dict(cluster=1, max_m=mmax, block=False)
     if ld * nmax <= SVD_SMEM_DOUBLES and (nmax + 1) // 2 <= SVD_SINGLE_MAX_PAIRS:
@@ -1043,11 +1055,14 @@ def retune_clusters(builder, rk, margin=1.1):
         n2 = min(int(nn * margin) + 1, m2) if nn else 0
         G = svd_cluster_runtime(len(probs), m2, n2)
         block = svd_use_block(len(probs), m2, n2, G)
+        bG = svd_block_cluster(len(probs), n2) if block else 1
         if block:
             G = 1
-        if G != extra.get("cluster", 1) or block != extra.get("block", False):
+        if (G != extra.get("cluster", 1) or block != extra.get("block", False)
+                or bG != extra.get("bcluster", 1)):
             extra["cluster"] = G
             extra["block"] = block
+            extra["bcluster"] = bG
             changed += 1
     return changed
 
@@ -1393,7 +1408,7 @@ class CompiledPlan:
                 rc = lib.hq_qr(stream_handle, dp + o1, cnt, rk, ex.get("cluster", 1))
             elif kind == "svd":
                 if ex.get("block"):
-                    rc = lib.hq_svd_block(stream_handle, dp + o1, cnt, rk, sc)
+                    rc = lib.hq_svd_block(stream_handle, dp + o1, cnt, rk, sc, ex.get("bcluster", 1))
                 else:
                     rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0))
             elif kind == "applyq":

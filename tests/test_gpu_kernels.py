@@ -268,11 +268,11 @@ def test_svd_truncation(dev, m, n, keep, xform, CL):
     assert err <= thr * 1.0001 + 1e-12 * np.linalg.norm(C, 2)
 
 
-@pytest.mark.parametrize("xform", [0, 1])
+@pytest.mark.parametrize("xform,G", [(0, 1), (1, 1), (1, 2), (1, 4), (1, 8)])
 @pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60),
                                       (200, 190, 120), (256, 256, 200), (130, 128, 128), (448, 448, 300),
                                       (600, 300, 250), (640, 200, 150), (97, 33, 30), (17, 17, 1)])
-def test_svd_block_truncation(dev, m, n, keep, xform):
+def test_svd_block_truncation(dev, m, n, keep, xform, G):
     """hq_svd_block (block Jacobi on the tensor pipe): same contract as
     hq_svd -- rank by the threshold, orthonormal U_k spanning the kept
     singular subspace -- on graded spectra down to 1e-14."""
@@ -297,7 +297,7 @@ def test_svd_block_truncation(dev, m, n, keep, xform):
     p = np.zeros(1, _abi.SVD_PROB)
     p[0] = (dC.data_ptr(), dU.data_ptr(), dW.data_ptr(), ldc, m, m, -1, n, -1, min(m, n), 0, 1, -1, thr, xform, 0)
     dp = put(torch, p)
-    assert lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr()) == 0
+    assert lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), G) == 0
     torch.cuda.synchronize()
     k = int(rank[0].item())
     assert int(rank[1].item()) == 0, "capacity flag"
@@ -308,6 +308,6 @@ def test_svd_block_truncation(dev, m, n, keep, xform):
     assert err <= thr * 1.0001 + 1e-12 * np.linalg.norm(C, 2)
     # deterministic: a second launch gives the same U bit for bit
     U1 = back(dU, m, min(m, n)).copy()
-    assert lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr()) == 0
+    assert lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), G) == 0
     torch.cuda.synchronize()
     assert np.array_equal(back(dU, m, min(m, n)), U1)

@@ -6,7 +6,7 @@ import sys
 sys.path.insert(0, ".")
 import numpy as np, torch
 from paper_1809_10585_b200 import _abi
-from paper_1809_10585_b200.plan import svd_cluster_runtime
+from paper_1809_10585_b200.plan import svd_block_cluster, svd_cluster_runtime
 lib = _abi.load()
 sizes = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [64, 100, 150, 200, 300, 450, 560]
 P = int(sys.argv[2]) if len(sys.argv) > 2 else 56
@@ -38,7 +38,7 @@ for n in sizes:
     res = {}
     G = svd_cluster_runtime(P, n, n)
     for name, fn in (("scalar G=%d" % G, lambda: lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), G, n)),
-                     ("block", lambda: lib.hq_svd_block(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr()))):
+                     ("block", lambda: lib.hq_svd_block(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), svd_block_cluster(P, n)))):
         fn(); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()

@@ -11,6 +11,7 @@ os.environ["HQ_LIB"] = "tools/libhq_dbg.so"
 import importlib
 import numpy as np, torch
 from paper_1809_10585_b200 import _abi
+from paper_1809_10585_b200.plan import svd_block_cluster
 _abi.LIB_PATH = "tools/libhq_dbg.so"
 lib = _abi.load(build_if_missing=False)
 sizes = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [100, 150, 300]
@@ -41,6 +42,6 @@ for n in sizes:
         if name == "scalar":
             lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), 1, n)
         else:
-            lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr())
+            lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), svd_block_cluster(1, n))
         e1.record(); torch.cuda.synchronize()
         print(n, name, "ms %.3f" % e0.elapsed_time(e1), "rank", int(rank[0]), "sweeps", int(rank[2]), flush=True)
