@@ -35,7 +35,7 @@ struct BjWarp {
 struct BjSmem {
   BjWarp w[BJ_NW];
   double nrm[MAX_N];
-  int rotf[2];
+  int rotf[3];   // per-sweep flags, slot sweep % 3 (see svd_block_body)
   int cnt;
 };
 
@@ -285,7 +285,7 @@ __device__ void svd_block_body(const hq_svd_prob& Pin, int* __restrict__ rank, c
     X[e] = P.xform ? ((i < m && j <= i) ? P.c[j + (size_t)i * P.ldc] : 0.0)
                    : (i < m ? P.c[i + (size_t)j * P.ldc] : 0.0);
   }
-  if (t < 2) S.rotf[t] = 0;
+  if (t < 3) S.rotf[t] = 0;
   bj_sync<G>();
   const double tol = 4.0 * sqrt((double)m) * 2.220446049250313e-16;
   const double tol2 = tol * tol, thr2 = thr * thr, tiny2 = (1e-3 * thr) * (1e-3 * thr);
@@ -297,21 +297,28 @@ __device__ void svd_block_body(const hq_svd_prob& Pin, int* __restrict__ rank, c
 #ifdef HQ_DEBUG_SWEEPS
     nsw = sweep + 1;
 #endif
-    if (t == 0) S.rotf[(sweep + 1) & 1] = 0;
+    // slot sweep % 3 collects this sweep's flag; the next sweep's slot is
+    // cleared now.  Three slots: a CTA that enters sweep s + 1 clears the
+    // slot of sweep s - 1, which every CTA of the cluster finished reading
+    // before the first barrier of sweep s (a CTA may still be reading the
+    // flags of sweep s, so two slots would race and let the CTAs disagree
+    // about termination)
+    const int fs = sweep % 3;
+    if (t == 0) S.rotf[(sweep + 1) % 3] = 0;
     for (int r = 0; r < nbp - 1; ++r) {
       for (int k = gw; k < ntask; k += G * BJ_NW) {
         int I, J;
         circle_pair(r, k, nbp, I, J);
         if (I >= nb) continue;   // both blocks are padding
-        if (bj_task(X, ld, m, n, I, J, tol2, tiny2, thr2, S.w[wid]) && lane == 0) S.rotf[sweep & 1] = 1;
+        if (bj_task(X, ld, m, n, I, J, tol2, tiny2, thr2, S.w[wid]) && lane == 0) S.rotf[fs] = 1;
       }
       bj_sync<G>();
     }
-    int any = S.rotf[sweep & 1];
+    int any = S.rotf[fs];
     if constexpr (G > 1) {
       cg::cluster_group cl = cg::this_cluster();
 #pragma unroll
-      for (int c = 0; c < G; ++c) any |= *cl.map_shared_rank(&S.rotf[sweep & 1], c);
+      for (int c = 0; c < G; ++c) any |= *cl.map_shared_rank(&S.rotf[fs], c);
     }
     if (!any) break;
   }
