@@ -19,7 +19,7 @@ eng.factorize(mats)
 eng.factorize(mats)
 rk = eng.h_rk_out.numpy()
 plan = eng.plan
-eng.pack(mats); eng.upload(); torch.cuda.synchronize()
+eng.pack(mats); eng.upload(); eng.stage_to_live(); torch.cuda.synchronize()
 s = eng.stream
 evs = []
 orig = plan.launch
