@@ -133,6 +133,23 @@ typedef struct hq_svd_prob {
   int32_t xform, pad_;
 } hq_svd_prob;
 
+/* column-pivoted Householder QR of a truncation core C (m x n, destroyed), R
+   only, stopped at the first step r where the remaining columns are
+   negligible: (n - r) max ||R22[:, c]||^2 <= (stop_scale * scal[eps_slot])^2
+   (eps_slot < 0: stop_scale^2; stop_scale = 0: only exactly zero columns
+   stop it).  Columns are not swapped: on exit rows 0..r-1 of c hold
+   [R11 R12] P^T in the original column order and r is in rank[r_ri]; with
+   hq_svd_prob.xform = 2 the Jacobi runs on X = (those rows)^T (n x r), whose
+   left singular vectors are those of C^T up to the dropped block.
+   (reference: the svd inside truncate_lowrank, core.py:250-253) */
+typedef struct hq_qrcp_prob {
+  double* c;
+  int32_t ldc;
+  int32_t m, m_ri, n, n_ri;
+  int32_t r_ri, eps_slot, pad_;
+  double stop_scale;
+} hq_qrcp_prob;
+
 /* a slab of reduced-away rows B_R of an ancestor (hqr.py:112,127) */
 typedef struct hq_slab {
   const double* v;   /* V factor rows for this leaf: element (i,c) = v[c + i*ld] */
@@ -182,7 +199,7 @@ typedef struct hq_rowblk_prob {
 /* ---- launchers ---------------------------------------------------------- */
 /* bumped whenever a descriptor layout or a launcher signature changes;
    the Python binding refuses a library with another version */
-#define HQ_ABI_VERSION 4
+#define HQ_ABI_VERSION 5
 int hq_abi_version(void);
 int hq_device_check(void);
 
@@ -241,6 +258,12 @@ int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const d
    barrier per round); 1: one CTA per problem. */
 int hq_svd_block(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal,
                  int cluster);
+/* cluster = 1, 2, 4 or 8 CTAs per problem (each holds a column slice in
+   shared memory); smem_doubles: dynamic shared memory per CTA in doubles
+   (2 ceil(n/G) + 2 G (m + 5) + m (ceil(n/G) + 15) holds an m x n core;
+   larger slices are reduced in place in global memory); threads: 256 or 512 */
+int hq_qrcp(void* stream, const hq_qrcp_prob* probs, int nprob, int* rank, const double* scal,
+            int cluster, int smem_doubles, int threads);
 int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,
                    int* rank, int max_nl);
 int hq_leaf_scatter(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,

@@ -38,6 +38,8 @@ SVD_PROB = np.dtype([("c", P), ("u", P), ("work", P), ("ldc", I), ("ldu", I), ("
                      ("m_ri", I), ("n", I), ("n_ri", I), ("cap", I), ("rank_ri", I),
                      ("flag_ri", I), ("eps_slot", I), ("eps_scale", np.float64),
                      ("xform", I), ("pad_", I)], align=True)
+QRCP_PROB = np.dtype([("c", P), ("ldc", I), ("m", I), ("m_ri", I), ("n", I), ("n_ri", I),
+                      ("r_ri", I), ("eps_slot", I), ("pad_", I), ("stop_scale", np.float64)], align=True)
 SLAB = np.dtype([("v", P), ("yv", P), ("ld", I), ("ldy", I), ("k_ri", I), ("pad_", I)], align=True)
 LEAF_PROB = np.dtype([("leaf", P), ("panel", P), ("nl", I), ("ldp", I), ("slab0", I),
                       ("nslab", I), ("m_ri", I), ("pad_", I)], align=True)
@@ -51,11 +53,11 @@ ROWBLK_PROB = np.dtype([("s", P), ("w", P), ("lds", I), ("ldw", I), ("ch", I), (
 
 STRUCT_SIZES = {"hq_rowblk_prob": ROWBLK_PROB, "hq_copy_item": COPY_ITEM, "hq_gemm_term": GEMM_TERM, "hq_gemm_prob": GEMM_PROB, "hq_piece": PIECE,
                 "hq_concat_prob": CONCAT_PROB, "hq_qr_prob": QR_PROB,
-                "hq_applyq_prob": APPLYQ_PROB, "hq_svd_prob": SVD_PROB, "hq_slab": SLAB,
+                "hq_applyq_prob": APPLYQ_PROB, "hq_svd_prob": SVD_PROB, "hq_qrcp_prob": QRCP_PROB, "hq_slab": SLAB,
                 "hq_leaf_prob": LEAF_PROB}
 
 EXPORTS = ("hq_abi_version", "hq_device_check", "hq_gemm", "hq_gemm_tiled", "hq_gemm_skinny", "hq_concat", "hq_qr", "hq_applyq",
-           "hq_svd", "hq_svd_block", "hq_leaf_gather", "hq_leaf_scatter", "hq_zero", "hq_power_step", "hq_copy",
+           "hq_svd", "hq_svd_block", "hq_qrcp", "hq_leaf_gather", "hq_leaf_scatter", "hq_zero", "hq_power_step", "hq_copy",
            "hq_pack_offsets", "hq_rowblocks")
 
 _vp, _i, _d, _i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
@@ -70,6 +72,7 @@ SIGNATURES = {
     "hq_applyq": [_vp, _vp, _i, _vp, _i],
     "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i],
     "hq_svd_block": [_vp, _vp, _i, _vp, _vp, _i],
+    "hq_qrcp": [_vp, _vp, _i, _vp, _vp, _i, _i, _i],
     "hq_leaf_gather": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_leaf_scatter": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_zero": [_vp, _vp, _i, _i64],
@@ -80,7 +83,7 @@ SIGNATURES = {
 }
 
 _LIB = None
-ABI_VERSION = 4   # HQ_ABI_VERSION in include/hodlrqr_b200.h
+ABI_VERSION = 5   # HQ_ABI_VERSION in include/hodlrqr_b200.h
 
 
 class LibraryError(RuntimeError):

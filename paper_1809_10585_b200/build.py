@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhqb200.so")
-SOURCES = ["hq_gemm.cu", "hq_qr.cu", "hq_svd.cu"]
+SOURCES = ["hq_gemm.cu", "hq_qr.cu", "hq_svd.cu", "hq_qrcp.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "--expt-relaxed-constexpr"]
 
@@ -29,7 +29,7 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile the three translation units in parallel (objects in a
+    """Compile the translation units in parallel (objects in a
     temporary directory), then link the shared library."""
     import tempfile
     if not force and not stale():

@@ -123,3 +123,36 @@ HQ_DEV void dmma_kloop(double& d0, double& d1, int kb, int ke, F fetch) {
     }
   }
 }
+
+// Reflector of the column x = [x0; v] (dense.py:45-68) from the sum of
+// squares ss of v (scaled by sc, see below), with the reference's sign
+// convention rho = -sign(x0) ||x||, sign(0) = +1, and gamma = 0 for x = 0.
+// The reference divides by max|x| before the norm.  Here the unscaled sum is
+// used whenever x0^2 + ss lies in [2^-900, 2^900]: then no square overflowed
+// and every square that underflowed is below 2^-112 of the total, so the
+// result equals the scaled one to rounding.  Otherwise (rare: zero or tiny
+// columns, overflow, inf/NaN) the column is rescaled by an exact power of two
+// sc chosen from max|x| and the sum recomputed.
+struct Refl { double gamma, rho, inv; };
+HQ_DEV bool refl_safe(double x0, double ss) {
+  const double tot = fma(x0, x0, ss);
+  return tot >= 0x1p-900 && tot <= 0x1p900;   // false for 0, inf and NaN
+}
+HQ_DEV double refl_scale(double amax) {
+  return amax < 0x1p-480 ? 0x1p600 : (amax > 0x1p480 ? 0x1p-600 : 1.0);
+}
+// isc = 1 / sc (exact: sc is a power of two)
+HQ_DEV Refl make_refl(double x0, double ss, double sc, double isc) {
+  Refl r{0.0, 0.0, 0.0};
+  const double xs = x0 * sc;
+  const double nrm = sqrt(fma(xs, xs, ss));
+  if (nrm != 0.0) {
+    const double sg = x0 < 0.0 ? -1.0 : 1.0;   // sign(0) := +1
+    const double u1 = xs + sg * nrm;           // no cancellation
+    r.rho = -sg * nrm * isc;
+    const double iu = 1.0 / u1;
+    r.inv = sc * iu;                           // y = v * inv
+    r.gamma = 2.0 / (1.0 + ss * iu * iu);
+  }
+  return r;
+}

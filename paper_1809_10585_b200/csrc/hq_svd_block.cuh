@@ -281,8 +281,8 @@ __device__ void svd_block_body(const hq_svd_prob& Pin, int* __restrict__ rank, c
   double* X = P.work;
   for (int e = cr * BJ_NT + t; e < ld * n; e += G * BJ_NT) {
     const int i = e % ld, j = e / ld;
-    // xform: X[i][j] = R[j][i] (j <= i), R stored in c with leading dim ldc
-    X[e] = P.xform ? ((i < m && j <= i) ? P.c[j + (size_t)i * P.ldc] : 0.0)
+    // xform: X[i][j] = R[j][i] (1: j <= i, 2: all), R stored in c with leading dim ldc
+    X[e] = P.xform ? ((i < m && (j <= i || P.xform == 2)) ? P.c[j + (size_t)i * P.ldc] : 0.0)
                    : (i < m ? P.c[i + (size_t)j * P.ldc] : 0.0);
   }
   if (t < 3) S.rotf[t] = 0;

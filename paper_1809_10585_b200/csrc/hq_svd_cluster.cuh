@@ -67,7 +67,7 @@ __device__ __noinline__ void svd_cluster_body(const hq_svd_prob& P, int* __restr
       double* dst = blk(0, slot) + (size_t)jj * ld;
       for (int i = t; i < ld; i += CNT) {
         double v = 0.0;
-        if (j < n && i < m) v = P.xform ? (j <= i ? P.c[j + (size_t)i * P.ldc] : 0.0)
+        if (j < n && i < m) v = P.xform ? ((j <= i || P.xform == 2) ? P.c[j + (size_t)i * P.ldc] : 0.0)
                                         : P.c[i + (size_t)j * P.ldc];
         dst[i] = v;
       }

@@ -299,10 +299,10 @@ __device__ __noinline__ void svd_single(const hq_svd_prob& Pin, int* __restrict_
   else if (P.xform) { X = P.work; ld = m; }
   else { X = P.c; ld = P.ldc; }
   if (P.xform) {
-    // X[i][j] = R[j][i] (j <= i), R stored in c with leading dim ldc
+    // X[i][j] = R[j][i] (xform 1: j <= i, 2: all), R stored in c with leading dim ldc
     for (int e = t; e < m * n; e += NT) {
       const int i = e % m, j = e / m;
-      X[i + (size_t)j * ld] = j <= i ? P.c[j + (size_t)i * P.ldc] : 0.0;
+      X[i + (size_t)j * ld] = (j <= i || P.xform == 2) ? P.c[j + (size_t)i * P.ldc] : 0.0;
     }
   } else if (staged) {
     for (int e = t; e < m * n; e += NT) X[e % m + (size_t)(e / m) * ld] = P.c[e % m + (size_t)(e / m) * P.ldc];

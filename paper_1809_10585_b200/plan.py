@@ -525,6 +525,7 @@ class Builder:
         z = self.lane_bump(R_TRUNC)
         z.reset()
         cat, qr, stack, qrs, gm_c, qrc, svd, apq, unstack, apq2, gm_m, gm_v = ([] for _ in range(12))
+        pivot = PIVOT_CORE
         maxrows, maxch = 0, 0
 
         def factor_side(W, rows, kcap, kri, tau, tp):
@@ -571,13 +572,23 @@ class Builder:
             maxrows = max(maxrows, m, n)
             (R1, ld1), tsL = factor_side(WL, m, kcap, kL, tauL, tpL)
             (R2, ld2), _ = factor_side(WR, n, kcap, kR, tauR, tpR)
-            # C^T = R2 R1^T (masks: upper on the stored R factors); its QR gives
-            # the LQ preconditioner X = R_c^T of C (Jacobi converges in few sweeps)
+            # C^T = R2 R1^T (masks: upper on the stored R factors).  Its
+            # column-pivoted QR, stopped where the remaining columns are below
+            # 1e-3 of the threshold (Frobenius norm), leaves r rows of R; the
+            # Jacobi runs on X = (those rows)^T (k1 x r): graded, r close to
+            # the rank instead of min(k1, k2) columns, few sweeps.  Without
+            # pivoting (HQ_PIVOT_CORE=0): X = R_c^T of the plain QR.
             gm_c.append((C, k2, Dim(k2, kR), Dim(k1, kL), 0.0,
                          [(R2, ld2, 0, 1, R1, ld1, 1, 1, Dim(kcap, kL), 1.0)]))
-            qrc.append((C, tauC, tpC, None, k2, 0, Dim(k2, kR), Dim(k1, kL)))
-            svd.append((C, Uk, Xw, k2, k1, Dim(k1, kL), Dim(k2, kR), cap, p["rank_ri"],
-                        p.get("flag", self.flag_slot), p["eps_slot"], p["eps_scale"], 1))
+            if pivot:
+                rC = self.slots.take()
+                qrc.append((C, k2, Dim(k2, kR), Dim(k1, kL), rC, p["eps_slot"], CORE_STOP * p["eps_scale"]))
+                svd.append((C, Uk, Xw, k2, k1, Dim(k1, kL), Dim(min(k1, k2), rC), cap, p["rank_ri"],
+                            p.get("flag", self.flag_slot), p["eps_slot"], p["eps_scale"], 2))
+            else:
+                qrc.append((C, tauC, tpC, None, k2, 0, Dim(k2, kR), Dim(k1, kL)))
+                svd.append((C, Uk, Xw, k2, k1, Dim(k1, kL), Dim(k2, kR), cap, p["rank_ri"],
+                            p.get("flag", self.flag_slot), p["eps_slot"], p["eps_scale"], 1))
             U, ldu = p["U"]
             V, ldv = p["V"]
             if tsL is None:
@@ -605,7 +616,11 @@ class Builder:
             self.op("rowblk", stack, dict(max_chunks=maxch))
             self.op("qr", qrs, dict(role="tsqr"))
         self.gemm(gm_c)
-        self.op("qr", qrc, dict(role="core"))
+        if pivot:
+            G, smem, threads = qrcp_launch(len(qrc), max(p[2].cap for p in qrc), max(p[3].cap for p in qrc))
+            self.op("qrcp", qrc, dict(cluster=G, smem=smem, threads=threads))
+        else:
+            self.op("qr", qrc, dict(role="core"))
         self.op("svd", svd, svd_cluster(svd))
         self.op("applyq", apq, dict(max_cols=max(p[10].cap for p in apq)))
         if unstack:
@@ -933,6 +948,9 @@ class Builder:
 
 # ---------------------------------------------------------------- packing
 
+PIVOT_CORE = os.environ.get("HQ_PIVOT_CORE", "1") != "0"   # column-pivoted core QR before the Jacobi
+CORE_STOP = 1e-3           # pivoted QR stops at ||R22||_F <= CORE_STOP * threshold (the Jacobi's own
+                           # level for columns it never rotates against each other)
 SVD_SMEM_DOUBLES = 24576   # single-CTA staging capacity (hq_svd_kernel.cuh)
 CLUSTER_BUF_DOUBLES = 26880  # per-CTA block buffers (hq_svd_cluster.cuh C_SMEM_DOUBLES)
 SVD_SINGLE_MAX_PAIRS = 16     # HQ_SVD_SINGLE_MAX_PAIRS (hq_svd_cluster.cuh)
@@ -1017,6 +1035,43 @@ def _svd_fits(G, m, n):
     return m <= 640 and 4 * bs * ((m + 1) // 2 * 2) <= SVD_C_SMEM_DOUBLES and bs <= SVD_C_MAX_BS
 
 
+QRCP_SMEM_MAX = 28928   # doubles of dynamic shared memory per CTA (hq_qrcp.cu)
+
+
+def qrcp_smem(G, m, n, threads):
+    """Shared-memory doubles a CTA of a G-CTA hq_qrcp cluster needs to hold
+    its column slice of an m x n core (the kernel's own carve-up: norms,
+    candidate buffers, the slice with its bank-staggered row stride), or None
+    when the slice cannot live there."""
+    ncl = -(-n // G)
+    tpc = 1
+    while tpc < 32 and ncl * tpc * 2 <= threads:
+        tpc *= 2
+    if ncl * tpc > threads:
+        return None
+    q = 32 // tpc if tpc >= 4 else 0
+    lds = ncl + (q - ncl) % 16
+    need = 2 * ncl + 2 * G * (((m + 1) & ~1) + 4) + m * lds
+    return need if need <= QRCP_SMEM_MAX else None
+
+
+def qrcp_launch(nprob, m, n, sms=148):
+    """(cluster size, shared-memory doubles, threads) of a pivoted-QR launch
+    whose largest core is m x n: the smallest cluster that holds the core in
+    shared memory, widened while the launch still fits one wave; many small
+    cores run 256-thread CTAs, several per SM."""
+    if m <= 0 or n <= 0:
+        return 1, 64, 256
+    threads = 256 if (n <= 64 and nprob > sms) else 512
+    fit = [G for G in (1, 2, 4, 8) if qrcp_smem(G, m, n, threads)]
+    if not fit:
+        return 8, QRCP_SMEM_MAX, 512   # reduced in place in global memory
+    G = fit[0]
+    while G < 8 and nprob * 2 * G <= sms and n >= 32 * G:
+        G *= 2
+    return G, qrcp_smem(G, m, n, threads), threads
+
+
 def svd_cluster_runtime(nprob, m, n, sms=148):
     """Cluster size for a Jacobi launch whose largest core is m x n (run-time
     sizes, e.g. from a previous run of the plan): the smallest cluster whose
@@ -1043,6 +1098,16 @@ def retune_clusters(builder, rk, margin=1.1):
     re-captures its graph)."""
     changed = 0
     for kind, probs, extra in builder.ops:
+        if kind == "qrcp" and probs:
+            mm = max(_dv(p[2], rk) for p in probs)
+            nn = max(_dv(p[3], rk) for p in probs)
+            m2 = min(int(mm * margin) + 1, max(p[2].cap for p in probs)) if mm else 0
+            n2 = min(int(nn * margin) + 1, max(p[3].cap for p in probs)) if nn else 0
+            G, smem, threads = qrcp_launch(len(probs), m2, n2)
+            if (G, smem, threads) != (extra.get("cluster"), extra.get("smem"), extra.get("threads")):
+                extra["cluster"], extra["smem"], extra["threads"] = G, smem, threads
+                changed += 1
+            continue
         if kind != "svd" or not probs:
             continue
         mm = nn = 0
@@ -1123,6 +1188,11 @@ def op_resources(builder, kind, probs, extra, mem=None):
     elif kind == "qr":
         for (w, tau, tp, tf, ldw, ldt, m, k) in probs:
             rd(w), wr(w), wr(tau), wr(tp), wr(tf), slot(m), slot(k)
+    elif kind == "qrcp":
+        for (c, ldc, m, n, rri, es, ssc) in probs:
+            rd(c), wr(c), slot(m), slot(n), slot(rri, True)
+            if es >= 0:
+                R.add(("scal",))
     elif kind == "svd":
         for (c, u, w, ldc, ldu, m, n, cap, rri, fri, es, esc, xf) in probs:
             rd(c), wr(c), wr(u), wr(w), slot(m), slot(n), slot(rri, True)
@@ -1296,6 +1366,11 @@ class CompiledPlan:
                 for i, (w, tau, tp, tf, ldw, ldt, m, k) in enumerate(probs):
                     pa[i] = (A(w), A(tau), A(tp), A(tf), ldw, ldt, m.cap, m.ri, k.cap, k.ri)
                 self.launch.append(("qr", put(pa), None, len(probs), extra))
+            elif kind == "qrcp":
+                pa = np.zeros(len(probs), _abi.QRCP_PROB)
+                for i, (c, ldc, m, n, rri, es, ssc) in enumerate(probs):
+                    pa[i] = (A(c), ldc, m.cap, m.ri, n.cap, n.ri, rri, es, 0, ssc)
+                self.launch.append(("qrcp", put(pa), None, len(probs), extra))
             elif kind == "svd":
                 pa = np.zeros(len(probs), _abi.SVD_PROB)
                 for i, (c, u, w, ldc, ldu, m, n, cap, rri, fri, es, esc, xf) in enumerate(probs):
@@ -1406,6 +1481,9 @@ class CompiledPlan:
                 rc = lib.hq_concat(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_rows"])
             elif kind == "qr":
                 rc = lib.hq_qr(stream_handle, dp + o1, cnt, rk, ex.get("cluster", 1))
+            elif kind == "qrcp":
+                rc = lib.hq_qrcp(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1),
+                                 ex.get("smem", QRCP_SMEM_MAX), ex.get("threads", 512))
             elif kind == "svd":
                 if ex.get("block"):
                     rc = lib.hq_svd_block(stream_handle, dp + o1, cnt, rk, sc, ex.get("bcluster", 1))
@@ -1465,6 +1543,10 @@ def op_flops(kind, probs, rk):
             mm, kk, cc = _dv(p[8], rk), _dv(p[9], rk), _dv(p[10], rk)
             r = min(mm, kk)
             f += 4.0 * mm * r * cc - 2.0 * r * r * cc
+    elif kind == "qrcp":
+        for (c, ldc, m, n, rri, es, ssc) in probs:
+            mm, nn, r = _dv(m, rk), _dv(n, rk), int(rk[rri])
+            f += 4.0 * (mm * nn * r - (mm + nn) * r * r / 2.0 + r ** 3 / 3.0)
     elif kind == "svd":
         for p in probs:
             mm, nn = _dv(p[5], rk), _dv(p[6], rk)

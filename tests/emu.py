@@ -149,6 +149,36 @@ class Emu:
             if p["tfull"]:
                 self.mat(p["tfull"], p["ldt"], r, r)[:] = T
 
+    def qrcp(self, o1, cnt, ex):
+        """hq_qrcp: Businger-Golub pivoted Householder QR without column
+        swaps, stopped when (n - j) max ||remaining column||^2 <= stop^2; rows
+        0..r-1 keep [R11 R12] P^T, r goes to the rank table."""
+        for p in self.arr(o1, _abi.QRCP_PROB, cnt):
+            m, n = self.dim(p["m"], p["m_ri"]), self.dim(p["n"], p["n_ri"])
+            if m <= 0 or n <= 0:
+                self.rank[p["r_ri"]] = 0
+                continue
+            stop = p["stop_scale"] * (self.scal[p["eps_slot"]] if p["eps_slot"] >= 0 else 1.0)
+            C = self.mat(p["c"], p["ldc"], m, n)
+            done = np.zeros(n, bool)
+            r = min(m, n)
+            for j in range(min(m, n)):
+                nr = np.sqrt((C[j:] * C[j:]).sum(0))
+                nr[done] = -1.0
+                c = int(np.argmax(nr))
+                if nr[c] <= 0.0 or (n - j) * nr[c] ** 2 <= stop * stop:
+                    r = j
+                    break
+                g, rho, inv = self.house(C[j:, c].copy())
+                y = np.concatenate([[1.0], C[j + 1:, c] * inv])
+                rest = ~done
+                rest[c] = False
+                C[j:, rest] -= g * np.outer(y, y @ C[j:, rest])
+                C[j, c] = rho
+                C[j + 1:, c] = 0.0
+                done[c] = True
+            self.rank[p["r_ri"]] = r
+
     def applyq(self, o1, cnt, ex):
         for p in self.arr(o1, _abi.APPLYQ_PROB, cnt):
             m, k = self.dim(p["m"], p["m_ri"]), self.dim(p["k"], p["k_ri"])
@@ -178,7 +208,8 @@ class Emu:
                 continue
             if p["xform"]:
                 n = min(n, m)
-                X = np.triu(self.mat(p["c"], p["ldc"], n, m)).T
+                R = self.mat(p["c"], p["ldc"], n, m)
+                X = (R if p["xform"] == 2 else np.triu(R)).T
             else:
                 X = self.mat(p["c"], p["ldc"], m, n)
             u, s, _ = np.linalg.svd(X, full_matrices=False)
@@ -340,6 +371,8 @@ class Emu:
                 self.concat(o1, o2, cnt, ex)
             elif kind == "qr":
                 self.qr(o1, cnt, ex)
+            elif kind == "qrcp":
+                self.qrcp(o1, cnt, ex)
             elif kind == "applyq":
                 self.applyq(o1, cnt, ex)
             elif kind == "svd":

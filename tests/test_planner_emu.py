@@ -107,7 +107,7 @@ def test_svd_cluster_sizes_from_runtime_sizes():
 
 def test_retune_clusters_uses_the_rank_table():
     """After a run the Jacobi launches are re-sized from the core sizes in the
-    rank table (not the capacities), and only the svd ops change."""
+    rank table (not the capacities), and only the svd and pivoted-QR ops change."""
     from paper_1809_10585_b200.plan import retune_clusters
     a = gen.gen_random_hodlr(1024, 128, 16, 8.0, seed=0)
     (f,), io, plan = emulate([a], 1e-10)
@@ -115,7 +115,11 @@ def test_retune_clusters_uses_the_rank_table():
     before = [dict(ex) for _, _, ex in io.builder.ops]
     retune_clusters(io.builder, rk)
     for (kind, probs, ex), old in zip(io.builder.ops, before):
-        if kind != "svd":
+        if kind == "qrcp":
+            assert ex["cluster"] in (1, 2, 4, 8) and ex["threads"] in (256, 512)
+            assert {k: v for k, v in ex.items() if k not in ("cluster", "smem", "threads")} == \
+                {k: v for k, v in old.items() if k not in ("cluster", "smem", "threads")}
+        elif kind != "svd":
             assert ex == old
         else:
             assert ex["cluster"] in (1, 2, 4, 8)

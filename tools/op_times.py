@@ -38,6 +38,9 @@ def shape(kind, probs):
         return ""
     if kind == "qr":
         return "m%d k%d" % (max(_dv(p[6], rk) for p in probs), max(_dv(p[7], rk) for p in probs))
+    if kind == "qrcp":
+        return "m%d n%d r%d" % (max(_dv(p[2], rk) for p in probs), max(_dv(p[3], rk) for p in probs),
+                                max(int(rk[p[4]]) for p in probs))
     if kind == "svd":
         return "m%d n%d" % (max(_dv(p[5], rk) for p in probs), max(_dv(p[6], rk) for p in probs))
     if kind == "applyq":
@@ -58,6 +61,8 @@ with open(out, "w") as fh:
         key = ex.get("role", "") if isinstance(ex, dict) else ""
         if kind == "svd":
             key = "cl%s%s" % (ex.get("cluster", 1), "b%d" % ex.get("bcluster", 1) if ex.get("block") else "")
+        if kind == "qrcp":
+            key = "cl%s" % ex.get("cluster", 1)
         if kind == "gemm":
             key = "split%s" % ex.get("ksplit", 1)
         npb = len(probs) if isinstance(probs, (list, tuple)) else 0
