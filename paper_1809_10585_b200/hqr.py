@@ -420,6 +420,14 @@ class HQREngine(PlanIO):
             self.multi_stream = ms not in ("0", "")
         self._pins = []
         self._evs = []
+        # The plan is tens of millions of small Python objects (one tuple per
+        # kernel problem): a full collection of the cyclic GC walks them all
+        # (3.4 s for 57 matrices of n = 16384) and fires every few batches,
+        # triggered by the result trees' allocations.  They live as long as the
+        # engine, so they are moved to the permanent generation.
+        if os.environ.get("HQB200_GC_FREEZE", "1") not in ("0", ""):
+            import gc
+            gc.freeze()
 
     def _retune(self, rk):
         """After the first run, size the Jacobi clusters from the actual core
