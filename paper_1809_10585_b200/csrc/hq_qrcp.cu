@@ -44,6 +44,41 @@ __device__ __forceinline__ double* cp_remote(double* p, int r) {
   else return p;
 }
 
+// Reflector of x = [x0; v] from ss = sum v^2 (both in the safe range, see
+// refl_safe) with the hardware reciprocal / reciprocal square root refined
+// by Newton steps to full FP64 accuracy: ||x||, 1 / u1 and gamma = |u1| /
+// ||x|| (= 2 / (1 + ss / u1^2)) cost two short dependent chains instead of a
+// software sqrt and two divisions on the per-step critical path.
+HQ_DEV Refl cp_refl_fast(double x0, double ss) {
+  const double tot = fma(x0, x0, ss);
+  double rn;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(tot));
+  const double ht = 0.5 * tot;
+  rn = rn * fma(-ht * rn, rn, 1.5);
+  rn = rn * fma(-ht * rn, rn, 1.5);
+  double nrm = tot * rn;
+  nrm = fma(0.5 * rn, fma(-nrm, nrm, tot), nrm);
+  const double sg = x0 < 0.0 ? -1.0 : 1.0;
+  const double u1 = fma(sg, nrm, x0);
+  double iu;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(iu) : "d"(u1));
+  iu = iu * fma(-u1, iu, 2.0);
+  iu = iu * fma(-u1, iu, 2.0);
+  Refl r;
+  r.rho = -sg * nrm;
+  r.inv = iu;
+  r.gamma = fabs(u1) * rn;
+  return r;
+}
+
+// pivot key of a column: its squared norm's bit pattern (monotonic for
+// non-negative doubles) with the low 11 bits replaced by 2047 - local column
+// (a CTA owns at most 2047 columns): one 64-bit maximum picks the largest norm
+// (to 2^-41 relative) and, among equals, the lowest column.  0 = no column.
+HQ_DEV unsigned long long cp_key(double vn2, int col) {
+  return ((unsigned long long)__double_as_longlong(vn2) & ~0x7FFull) | (unsigned long long)(2047 - col);
+}
+
 template <int G>
 __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restrict__ rank,
                             const double* __restrict__ scal, int smem_doubles) {
@@ -63,25 +98,29 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
   const int ncl_max = (n + G - 1) / G, c0 = cr * ncl_max;
   const int ncl = max(0, min(ncl_max, n - c0));
   // threads per column (power of two) and the row stride that keeps the
-  // half-warps' accesses (TPC/2 rows x 32/TPC... columns) on distinct banks
+  // half-warps' accesses (a few rows x 32/TPC columns) on distinct banks
   int tpc = 1;
   while (tpc < 32 && ncl_max * tpc * 2 <= nt) tpc *= 2;
   const int cpw = 32 / tpc;                       // columns per warp
   const int q = tpc >= 4 ? 32 / tpc : 0;          // lds mod 16
   const int lds = ncl_max + ((q - ncl_max) % 16 + 16) % 16;
   const int mp = ((m + 1) & ~1) + CP_HDR;
-  double* vn = sm;                  // tracked column norms (< 0: column already a pivot)
-  double* vref = vn + ncl_max;      // norm at the last exact computation
+  unsigned long long* keymax = reinterpret_cast<unsigned long long*>(sm);   // [2] by step parity
+  double* vn = sm + 2;              // squared column norms, tracked (< 0: column already a pivot)
+  double* vref = vn + ncl_max;      // squared norm at the last exact computation
   double* cand = vref + ncl_max;    // [2][G][mp]: candidates by step parity and proposing CTA
   double* As = cand + 2 * G * mp;
-  const bool in_smem = ncl_max * tpc <= nt && (size_t)(As - sm) + (size_t)m * lds <= (size_t)smem_doubles;
+  const bool in_smem = ncl_max * tpc <= nt &&
+                       (size_t)(As - sm) + (size_t)m * lds <= (size_t)smem_doubles;
   double* Cg = P.c + (size_t)c0 * P.ldc;   // my slice in global memory
   const int ldc = P.ldc;
   // thread -> (column, row phase) of the shared-memory mode
   const int h = lane / cpw, cc = lane % cpw, col = wid * cpw + cc;
   const bool mine = col < ncl;
+  if (t < 2) keymax[t] = 0ull;
+  __syncthreads();
 
-  // ---- load the slice, exact column norms
+  // ---- load the slice, exact squared column norms, first pivot keys
   if (in_smem) {
     double ss = 0.0;
     if (mine) {
@@ -93,14 +132,14 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
       }
     }
     for (int o = cpw; o < 32; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (mine && h == 0) { const double nr = sqrt(ss); vn[col] = nr; vref[col] = nr; }
+    if (mine && h == 0) { vn[col] = ss; vref[col] = ss; atomicMax(&keymax[0], cp_key(ss, col)); }
   } else {
     for (int c = wid; c < ncl; c += nw) {
       const double* src = Cg + (size_t)c * ldc;
       double ss = 0.0;
       for (int i = lane; i < m; i += 32) ss = fma(src[i], src[i], ss);
       ss = warp_sum(ss);
-      if (lane == 0) { const double nr = sqrt(ss); vn[c] = nr; vref[c] = nr; }
+      if (lane == 0) { vn[c] = ss; vref[c] = ss; atomicMax(&keymax[0], cp_key(ss, c)); }
     }
   }
   __syncthreads();
@@ -110,42 +149,37 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
     double* mycand = cand + (size_t)((j & 1) * G + cr) * mp;
     // ---- phase A (warp 0): best local column and its reflector, to all CTAs
     if (wid == 0) {
-      double best = -1.0;
-      int bi = -1;
-      for (int c = lane; c < ncl; c += 32) {
-        const double v = vn[c];
-        if (v > best) { best = v; bi = c; }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
-      }
+      const unsigned long long key = keymax[j & 1];
+      const int bi = key ? 2047 - (int)(key & 0x7FFull) : -1;
+      const double best = bi >= 0 ? __longlong_as_double((long long)(key & ~0x7FFull)) : -1.0;
+      if (lane == 0) keymax[(j + 1) & 1] = 0ull;
       double gamma = 0.0, rho = 0.0, inv = 0.0;
       if (bi >= 0) {
         // raw column into my own candidate slot, sum of squares below the diagonal
-        double ss = 0.0, x0 = 0.0, amax = 0.0;
+        double ss = 0.0, x0 = 0.0;
         for (int i = j + lane; i < m; i += 32) {
           const double v = in_smem ? As[i * lds + bi] : Cg[(size_t)bi * ldc + i];
           mycand[CP_HDR + i] = v;
           if (i > j) ss = fma(v, v, ss); else x0 = v;
-          amax = fmax(amax, fabs(v));
         }
         ss = warp_sum(ss);
         x0 = __shfl_sync(0xffffffffu, x0, 0);
-        double sc = 1.0, isc = 1.0;
-        if (!refl_safe(x0, ss)) {   // warp-uniform, rare: rescale by max|x|
+        Refl R;
+        if (refl_safe(x0, ss)) {
+          R = cp_refl_fast(x0, ss);
+        } else {   // warp-uniform, rare: rescale by max|x| (zero, tiny or huge columns)
+          double amax = 0.0;
+          __syncwarp();
+          for (int i = j + lane; i < m; i += 32) amax = fmax(amax, fabs(mycand[CP_HDR + i]));
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-          sc = refl_scale(amax);
-          isc = sc == 1.0 ? 1.0 : (sc > 1.0 ? 0x1p-600 : 0x1p600);
+          const double sc = refl_scale(amax);
+          const double isc = sc == 1.0 ? 1.0 : (sc > 1.0 ? 0x1p-600 : 0x1p600);
           ss = 0.0;
-          __syncwarp();
           for (int i = j + 1 + lane; i < m; i += 32) { const double v = mycand[CP_HDR + i] * sc; ss = fma(v, v, ss); }
           ss = warp_sum(ss);
+          R = make_refl(x0, ss, sc, isc);
         }
-        const Refl R = make_refl(x0, ss, sc, isc);
         gamma = R.gamma; rho = R.rho; inv = R.inv;
       }
       __syncwarp();
@@ -171,59 +205,59 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
       const double b = hd[0], gc = hd[3];
       if (gc >= 0.0 && (b > wbest || (b == wbest && gc < wcol))) { wbest = b; wcol = gc; wc = c; }
     }
-    if (wcol < 0.0 || wbest == 0.0 || (double)(n - j) * wbest * wbest <= stop2) { r = j; break; }
+    if (wcol < 0.0 || wbest <= 0.0 || (double)(n - j) * wbest <= stop2) { r = j; break; }
     const double* wh = cand + (size_t)((j & 1) * G + wc) * mp;
     const double gamma = wh[1], rho = wh[2];
     const double* v = wh + CP_HDR;
     const int pc = wc == cr ? (int)wcol - c0 : -1;   // the pivot, if it is mine
+    unsigned long long* knext = &keymax[(j + 1) & 1];
     if (in_smem) {
-      const bool act = mine && col != pc && vn[col] >= 0.0;
+      const double vold = mine ? vn[col] : -1.0;
+      const bool act = mine && col != pc && vold >= 0.0;
       const int i0 = j + ((h - j) % tpc + tpc) % tpc;   // first row >= j with row = h (mod tpc)
       double* a = As + col;
-      double d0 = 0.0, d1 = 0.0;
+      const int st = tpc * lds;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
       if (act) {
         int i = i0;
-        for (; i + tpc < m; i += 2 * tpc) {
-          d0 = fma(v[i], a[i * lds], d0);
-          d1 = fma(v[i + tpc], a[(i + tpc) * lds], d1);
+        const double* ap = a + (size_t)i * lds;
+        for (; i + 3 * tpc < m; i += 4 * tpc, ap += 4 * st) {
+          d0 = fma(v[i], ap[0], d0);
+          d1 = fma(v[i + tpc], ap[st], d1);
+          d2 = fma(v[i + 2 * tpc], ap[2 * st], d2);
+          d3 = fma(v[i + 3 * tpc], ap[3 * st], d3);
         }
-        if (i < m) d0 = fma(v[i], a[i * lds], d0);
+        for (; i < m; i += tpc, ap += st) d0 = fma(v[i], ap[0], d0);
       }
-      double dot = d0 + d1;
+      double dot = (d0 + d1) + (d2 + d3);
       for (int o = cpw; o < 32; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
       const double tau = gamma * dot;
       double rj = 0.0;
       if (act) {
-        for (int i = i0; i < m; i += tpc) {
-          const double nv = fma(-tau, v[i], a[i * lds]);
-          a[i * lds] = nv;
-          if (i == j) rj = nv;
+        int i = i0;
+        double* ap = a + (size_t)i * lds;
+        if (i == j) { rj = fma(-tau, v[i], ap[0]); ap[0] = rj; i += tpc; ap += st; }
+        for (; i + tpc < m; i += 2 * tpc, ap += 2 * st) {
+          const double n0 = fma(-tau, v[i], ap[0]), n1 = fma(-tau, v[i + tpc], ap[st]);
+          ap[0] = n0; ap[st] = n1;
         }
+        if (i < m) ap[0] = fma(-tau, v[i], ap[0]);
       }
       rj = __shfl_sync(0xffffffffu, rj, (j % tpc) * cpw + cc);
-      // norm downdate (dgeqp3): exact recomputation when it cancels
-      bool redo = false;
-      double vnc = 0.0;
-      if (act) {
-        vnc = vn[col];
-        if (vnc > 0.0) {
-          double tt = fabs(rj) / vnc;
-          tt = fmax(0.0, (1.0 + tt) * (1.0 - tt));
-          const double rr = vnc / vref[col];
-          if (tt * rr * rr <= 1.4901161193847656e-08) redo = true;
-          else vnc *= sqrt(tt);
-        }
-      }
+      // squared-norm downdate with dgeqp3's safeguard: exact recomputation
+      // when the tracked value has cancelled to sqrt(eps) of the last exact one
+      double vnew = fmax(fma(-rj, rj, vold), 0.0);
+      const bool redo = act && vnew <= 1.4901161193847656e-08 * vref[col];
       if (__any_sync(0xffffffffu, redo)) {
         double ss = 0.0;
         if (redo)
-          for (int i = i0 + (i0 == j ? tpc : 0); i < m; i += tpc) ss = fma(a[i * lds], a[i * lds], ss);
+          for (int i = i0 + (i0 == j ? tpc : 0); i < m; i += tpc) ss = fma(a[(size_t)i * lds], a[(size_t)i * lds], ss);
         for (int o = cpw; o < 32; o <<= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (redo) { vnc = sqrt(ss); if (h == 0) vref[col] = vnc; }
+        if (redo) { vnew = ss; if (h == 0) vref[col] = ss; }
       }
-      if (act && h == 0) vn[col] = vnc;
+      if (act && h == 0) { vn[col] = vnew; atomicMax(knext, cp_key(vnew, col)); }
       if (mine && col == pc) {
-        for (int i = i0; i < m; i += tpc) a[i * lds] = i == j ? rho : 0.0;
+        for (int i = i0; i < m; i += tpc) a[(size_t)i * lds] = i == j ? rho : 0.0;
         if (h == 0) vn[col] = -1.0;
       }
     } else {
@@ -234,22 +268,19 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
           if (lane == 0) vn[c] = -1.0;
           continue;
         }
-        double vnc = vn[c];
-        if (vnc < 0.0) continue;
+        if (vn[c] < 0.0) continue;
         double dot = 0.0;
         for (int i = j + lane; i < m; i += 32) dot = fma(v[i], a[i], dot);
         dot = warp_sum(dot);
         const double tau = gamma * dot;
-        double rj = 0.0, ss = 0.0;
+        double ss = 0.0;   // the exact squared norm comes for free with the update pass
         for (int i = j + lane; i < m; i += 32) {
           const double nv = fma(-tau, v[i], a[i]);
           a[i] = nv;
-          if (i == j) rj = nv; else ss = fma(nv, nv, ss);
+          if (i > j) ss = fma(nv, nv, ss);
         }
-        // the exact norm comes for free with the update pass
-        (void)rj;
         ss = warp_sum(ss);
-        if (lane == 0) { vnc = sqrt(ss); vn[c] = vnc; vref[c] = vnc; }
+        if (lane == 0) { vn[c] = ss; atomicMax(knext, cp_key(ss, c)); }
       }
     }
     __syncthreads();

@@ -1051,7 +1051,7 @@ def qrcp_smem(G, m, n, threads):
         return None
     q = 32 // tpc if tpc >= 4 else 0
     lds = ncl + (q - ncl) % 16
-    need = 2 * ncl + 2 * G * (((m + 1) & ~1) + 4) + m * lds
+    need = 2 + 2 * ncl + 2 * G * (((m + 1) & ~1) + 4) + m * lds
     return need if need <= QRCP_SMEM_MAX else None
 
 
