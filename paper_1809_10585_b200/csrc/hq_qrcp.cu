@@ -106,7 +106,8 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
   const int lds = ncl_max + ((q - ncl_max) % 16 + 16) % 16;
   const int mp = ((m + 1) & ~1) + CP_HDR;
   unsigned long long* keymax = reinterpret_cast<unsigned long long*>(sm);   // [2] by step parity
-  double* vn = sm + 2;              // squared column norms, tracked (< 0: column already a pivot)
+  double* bc = sm + 2;              // my candidate's header + 1 / u1, warp 0 -> all threads
+  double* vn = sm + 8;              // squared column norms, tracked (< 0: column already a pivot)
   double* vref = vn + ncl_max;      // squared norm at the last exact computation
   double* cand = vref + ncl_max;    // [2][G][mp]: candidates by step parity and proposing CTA
   double* As = cand + 2 * G * mp;
@@ -182,17 +183,31 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
         }
         gamma = R.gamma; rho = R.rho; inv = R.inv;
       }
-      __syncwarp();
-      // the local copy goes last: it overwrites the raw column the others are scaled from
-      for (int rr = G - 1; rr >= 0; --rr) {
-        const int dst = (cr + rr) % G;
-        double* rc = cp_remote<G>(mycand, dst);
+      if constexpr (G == 1) {
+        __syncwarp();
         if (bi >= 0)
-          for (int i = j + lane; i < m; i += 32) {
-            const double v = mycand[CP_HDR + i];
-            rc[CP_HDR + i] = i > j ? v * inv : 1.0;
-          }
-        if (lane == 0) { rc[0] = best; rc[1] = gamma; rc[2] = rho; rc[3] = bi >= 0 ? (double)(c0 + bi) : -1.0; }
+          for (int i = j + lane; i < m; i += 32) mycand[CP_HDR + i] = i > j ? mycand[CP_HDR + i] * inv : 1.0;
+        if (lane == 0) { mycand[0] = best; mycand[1] = gamma; mycand[2] = rho; mycand[3] = bi >= 0 ? (double)(c0 + bi) : -1.0; }
+      } else if (lane == 0) {
+        bc[0] = best; bc[1] = gamma; bc[2] = rho; bc[3] = bi >= 0 ? (double)(c0 + bi) : -1.0; bc[4] = inv;
+      }
+    }
+    if constexpr (G > 1) {
+      // every thread takes part in the broadcast of the scaled reflector:
+      // one thread per row writes its value to all G copies (its own last)
+      __syncthreads();
+      const double inv = bc[4];
+      if (bc[3] >= 0.0) {
+        for (int i = j + t; i < m; i += nt) {
+          const double sv = i > j ? mycand[CP_HDR + i] * inv : 1.0;
+#pragma unroll
+          for (int rr = 1; rr < G; ++rr) cp_remote<G>(mycand, (cr + rr) % G)[CP_HDR + i] = sv;
+          mycand[CP_HDR + i] = sv;
+        }
+      }
+      if (t < G) {
+        double* rc = cp_remote<G>(mycand, (cr + t) % G);
+        rc[0] = bc[0]; rc[1] = bc[1]; rc[2] = bc[2]; rc[3] = bc[3];
       }
     }
     cp_sync<G>();

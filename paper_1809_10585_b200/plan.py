@@ -1051,25 +1051,27 @@ def qrcp_smem(G, m, n, threads):
         return None
     q = 32 // tpc if tpc >= 4 else 0
     lds = ncl + (q - ncl) % 16
-    need = 2 + 2 * ncl + 2 * G * (((m + 1) & ~1) + 4) + m * lds
+    need = 8 + 2 * ncl + 2 * G * (((m + 1) & ~1) + 4) + m * lds
     return need if need <= QRCP_SMEM_MAX else None
 
 
 def qrcp_launch(nprob, m, n, sms=148):
     """(cluster size, shared-memory doubles, threads) of a pivoted-QR launch
     whose largest core is m x n: the smallest cluster that holds the core in
-    shared memory, widened while the launch still fits one wave; many small
-    cores run 256-thread CTAs, several per SM."""
+    shared memory (a step costs one cluster barrier and G candidate
+    broadcasts, so wider is slower: tools/qrcp_micro.py), two CTAs for cores
+    of >= 96 columns while the launch fits one wave; 512-thread CTAs when
+    every CTA gets its own SM, else 256 so that several share one."""
     if m <= 0 or n <= 0:
         return 1, 64, 256
-    threads = 256 if (n <= 64 and nprob > sms) else 512
-    fit = [G for G in (1, 2, 4, 8) if qrcp_smem(G, m, n, threads)]
-    if not fit:
-        return 8, QRCP_SMEM_MAX, 512   # reduced in place in global memory
-    G = fit[0]
-    while G < 8 and nprob * 2 * G <= sms and n >= 32 * G:
-        G *= 2
-    return G, qrcp_smem(G, m, n, threads), threads
+    for G in (1, 2, 4, 8):
+        threads = 512 if nprob * G <= sms else 256
+        if G == 1 and n >= 96 and nprob * 2 <= sms and qrcp_smem(2, m, n, 512):
+            continue
+        need = qrcp_smem(G, m, n, threads)
+        if need:
+            return G, need, threads
+    return 8, QRCP_SMEM_MAX, 512   # reduced in place in global memory
 
 
 def svd_cluster_runtime(nprob, m, n, sms=148):
