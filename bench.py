@@ -230,7 +230,23 @@ def instrument(eng, torch):
     return per, skipped
 
 
-def auto_batch(torch, ci, n, tol, local, cap=64, kcap=192, stream_out=True):
+BATCH_CAP = int(os.environ.get("HQ_BENCH_BATCH_CAP", "74"))   # 74 two-CTA clusters fill the 148 SMs
+
+
+def kcap_profile(cfg, tree, top=192):
+    """Rank capacity per tree level for a rank-k input (root = 0): 2 k (l + 1),
+    at most `top` -- the factors' ranks grow with the depth (measured over the
+    bench seeds, tools/level_ranks.py: at most 32/48/64/96/141/159 on levels
+    0..5 for k = 16), so the large top-level blocks are stored at their small
+    ranks and more matrices fit the HBM.  An overflow raises
+    RankCapacityError and the run is redone at a uniform 512."""
+    k = cfg.get("rank")
+    if not k:
+        return top
+    return tuple(min(top, 2 * k * (l + 1)) for l in range(max(tree.level, 1)))
+
+
+def auto_batch(torch, ci, n, tol, local, cap=None, kcap=192, stream_out=True):
     """Matrices per step: as many as fit 85 % of the free HBM (the arena of a
     one-matrix plan scales linearly with the batch), at most `cap`."""
     from paper_1809_10585_b200.gen import gen_config
@@ -242,7 +258,7 @@ def auto_batch(torch, ci, n, tol, local, cap=64, kcap=192, stream_out=True):
     ws = sum(b.peak for r, b in bld.bumps.items() if r % LANE_STRIDE == R_WS)
     per_matrix = 8 * (sum(b.peak for r, b in bld.bumps.items() if stream_out or r != R_OUT) - ws)
     free, _ = torch.cuda.mem_get_info(local)
-    return max(1, min(cap, int((0.85 * free - 8 * ws) / per_matrix)))
+    return max(1, min(cap or BATCH_CAP, int((0.85 * free - 8 * ws) / per_matrix)))
 
 
 def build_engine(torch, config, n, batch=None, kcap=None, local=0, ws=1, rank=0):
@@ -264,7 +280,9 @@ def build_engine(torch, config, n, batch=None, kcap=None, local=0, ws=1, rank=0)
         seeds = shard_seeds(total_batch, ws, rank)
         scaling = "strong"
     else:
-        per = batch or auto_batch(torch, config, n, cfg["tol"], local, kcap=kcap or 192)
+        tree0 = gen_config(config, seed=0, n=n).tree()
+        kc0 = kcap or kcap_profile(cfg, tree0)
+        per = batch or auto_batch(torch, config, n, cfg["tol"], local, kcap=kc0)
         seeds = list(range(rank * per, (rank + 1) * per))
         scaling = "weak"
     mats = [gen_config(config, seed=s, n=n) for s in seeds]
@@ -272,7 +290,7 @@ def build_engine(torch, config, n, batch=None, kcap=None, local=0, ws=1, rank=0)
     # rank capacity 192 (largest rank on this workload over 64 seeds: 159); an
     # overflow raises RankCapacityError -- it never truncates -- and the run
     # is redone at capacity 512 with the batch that fits
-    kc = kcap or (192 if total_batch == 1 else 512)
+    kc = kcap or (kc0 if total_batch == 1 else 512)
     while True:
         eng = HQREngine(a.tree(), len(mats), cfg["tol"], kcap=kc, device=f"cuda:{local}", stream_out=True)
         eng.pack(mats)
@@ -283,7 +301,7 @@ def build_engine(torch, config, n, batch=None, kcap=None, local=0, ws=1, rank=0)
             eng.download()
             break
         except RankCapacityError:
-            if kc >= 512:
+            if kc == 512:
                 raise
             del eng
             torch.cuda.empty_cache()

@@ -759,8 +759,13 @@ def clear_engines():
         pass
 
 
+def _kcap_key(kcap):
+    """Hashable form of a rank capacity (an int, or a per-level profile)."""
+    return int(kcap) if isinstance(kcap, (int, np.integer)) else tuple(int(k) for k in kcap)
+
+
 def engine_for(tree: PartitionTree, batch=1, eps=1e-10, absolute=False, kcap=512, use_graph=True):
-    key = (tuple(tree.leaf_sizes), batch, float(eps), bool(absolute), int(kcap), use_graph)
+    key = (tuple(tree.leaf_sizes), batch, float(eps), bool(absolute), _kcap_key(kcap), use_graph)
     eng = _ENGINES.get(key)
     if eng is not None:
         _ENGINES.move_to_end(key)
@@ -812,7 +817,7 @@ def hqr_rec(col, eps_abs: float, eps_plain: float, n_b: int = 32, kcap: int = 51
 
 
 def _rec_engine(tree, root_b, root_c, eps_plain, kcap):
-    key = ("rec", tuple(tree.leaf_sizes), root_b, root_c, float(eps_plain), int(kcap))
+    key = ("rec", tuple(tree.leaf_sizes), root_b, root_c, float(eps_plain), _kcap_key(kcap))
     eng = _ENGINES.get(key)
     if eng is not None:
         _ENGINES.move_to_end(key)

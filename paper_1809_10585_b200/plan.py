@@ -168,6 +168,16 @@ class Tree:
         return out
 
 
+def level_cap(kcap, level):
+    """Rank capacity of the blocks at a tree level (root = 0): kcap itself, or
+    entry `level` of a per-level profile (the last entry for deeper levels).
+    The factors' ranks grow with the depth (roughly input rank x level), so a
+    profile stores the large top-level blocks at their small ranks."""
+    if isinstance(kcap, (int, np.integer)):
+        return int(kcap)
+    return int(kcap[min(level, len(kcap) - 1)])
+
+
 class Layout:
     """Persistent per-matrix storage (see module docstring)."""
 
@@ -176,7 +186,7 @@ class Layout:
         self.kc = {}
         for u in self._all_internal():
             c1, c2 = tree.children(u)
-            self.kc[u] = max(1, min(tree.size[c1], tree.size[c2], kcap))
+            self.kc[u] = max(1, min(tree.size[c1], tree.size[c2], level_cap(kcap, u[0])))
         self.m = []
         for b in range(batch):
             d = {"leafA": {}, "leafT": {}, "A12U": {}, "A12V": {}, "A21U": {}, "A21V": {},

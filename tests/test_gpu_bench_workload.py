@@ -1,7 +1,8 @@
 """Parity of exactly what bench.py times (config 2, n = 16384): the engine is
 built by bench.build_engine -- the automatic batch (as many matrices as fit,
-<= 64), rank capacity 192, streaming output, Jacobi clusters re-tuned after
-the first run and the graph re-captured -- and its results are checked:
+<= 74), the per-level rank capacity profile (bench.kcap_profile, at most 192),
+streaming output, Jacobi / pivoted-QR clusters re-tuned after the first run
+and the graph re-captured -- and its results are checked:
 
 * matrix 0 against the reference's own full-size results
   (tests/golden/golden_full_cfg2.npz, produced by running hodlrqr): the R
@@ -48,7 +49,7 @@ def _floor():
 
 def test_timed_replays_are_bit_identical(bench_engine):
     torch, eng, mats, kcap = bench_engine
-    assert kcap == 192 and len(mats) >= 2
+    assert max(np.atleast_1d(kcap)) == 192 and len(mats) >= 2
     assert any(ex.get("cluster", 1) != 1 for k, _, ex in eng.builder.ops if k == "svd")
     outs = []
     for _ in range(2):
