@@ -245,9 +245,13 @@ int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank, int clust
 int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank, int max_cols);
 /* cluster >= 2: one-sided block Jacobi on a cluster of `cluster` CTAs (2, 4
    or 8) per problem, X distributed over their shared memories (DSMEM);
-   max_m bounds the row count (<= 512) and selects the lane-group width */
+   max_m bounds the row count (<= 512) and selects the lane-group width.
+   cluster = 1: one 512-thread CTA per problem.  cluster = 0: small cores,
+   one 128-thread CTA per problem with small_doubles doubles of staging
+   (>= ((m + 1) & ~1) * n of the largest core, else that core runs from
+   global memory), several CTAs per SM */
 int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank, const double* scal,
-           int cluster, int max_m);
+           int cluster, int max_m, int small_doubles);
 /* the same contract as hq_svd (one CTA per problem) by block one-sided
    Jacobi: blocks of 8 columns, per tournament round one warp per block pair
    forms the 16 x 16 Gram on the FP64 tensor pipe, diagonalizes it by
@@ -260,8 +264,9 @@ int hq_svd_block(void* stream, const hq_svd_prob* probs, int nprob, int* rank, c
                  int cluster);
 /* cluster = 1, 2, 4 or 8 CTAs per problem (each holds a column slice in
    shared memory); smem_doubles: dynamic shared memory per CTA in doubles
-   (2 ceil(n/G) + 2 G (m + 5) + m (ceil(n/G) + 15) holds an m x n core;
-   larger slices are reduced in place in global memory); threads: 256 or 512 */
+   (8 + 2 ceil(n/G) + 2 G (m + 5) for the norms and candidate buffers -- always
+   required -- plus m (ceil(n/G) + 15) for the slice of an m x n core; slices
+   that do not fit are reduced in place in global memory); threads: 256 or 512 */
 int hq_qrcp(void* stream, const hq_qrcp_prob* probs, int nprob, int* rank, const double* scal,
             int cluster, int smem_doubles, int threads);
 int hq_leaf_gather(void* stream, const hq_leaf_prob* probs, int nprob, const hq_slab* slabs,

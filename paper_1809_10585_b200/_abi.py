@@ -70,7 +70,7 @@ SIGNATURES = {
     "hq_concat": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_qr": [_vp, _vp, _i, _vp, _i],
     "hq_applyq": [_vp, _vp, _i, _vp, _i],
-    "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i],
+    "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i, _i],
     "hq_svd_block": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_qrcp": [_vp, _vp, _i, _vp, _vp, _i, _i, _i],
     "hq_leaf_gather": [_vp, _vp, _i, _vp, _vp, _i],

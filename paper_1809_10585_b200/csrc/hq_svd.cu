@@ -144,9 +144,23 @@ static int launch_cluster(cudaStream_t st, const hq_svd_prob* probs, int nprob, 
 }
 
 extern "C" int hq_svd(void* stream, const hq_svd_prob* probs, int nprob, int* rank,
-                      const double* scal, int cluster, int max_m) {
+                      const double* scal, int cluster, int max_m, int small_doubles) {
   if (nprob <= 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
+  if (cluster == 0) {
+    // small cores: 128-thread CTAs, small_doubles of staging each
+    static int attr_bytes = 0;
+    if (small_doubles < 64) small_doubles = 64;
+    if (small_doubles > SMEM_DOUBLES) small_doubles = SMEM_DOUBLES;
+    const int bytes = (int)offsetof(SvdSmem, cs) + 8 * small_doubles;
+    if (bytes > attr_bytes) {
+      cudaError_t e = cudaFuncSetAttribute(svd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e != cudaSuccess) return (int)e;
+      attr_bytes = bytes;
+    }
+    svd_small_kernel<<<nprob, SMALL_NT, bytes, st>>>(probs, rank, scal, small_doubles);
+    return hq_err(cudaGetLastError());
+  }
   if (cluster >= 2) {
     (void)max_m;  // cores past the cluster's limits run on CTA 0 (kernel-side test)
     if (cluster == 2) return launch_cluster<2>(st, probs, nprob, rank, scal);

@@ -15,8 +15,8 @@ constexpr int MAX_SWEEPS = 40;
 // fewer rounds, orthogonality of U unchanged).
 constexpr double QSTOP2 = 1e-14;
 
+// cs is last: the small-core kernel allocates only a prefix of it
 struct SvdSmem {
-  double cs[SMEM_DOUBLES];
   double nrm[MAX_N];
   short act[MAX_N];   // active columns (compaction of negligible ones)
   int nact;
@@ -27,6 +27,7 @@ struct SvdSmem {
   double2 trash[32];  // sink for the stores of rows past the column end
   int rot;
   int cnt;
+  alignas(16) double cs[SMEM_DOUBLES];   // staged X, 16-byte aligned columns
 };
 
 __device__ __forceinline__ void pair_of(int r, int pi, int N, int& p, int& q) {
@@ -160,12 +161,12 @@ __device__ __forceinline__ void compact_active(short* act, int& nact_out, const 
 // shuffles, the rotation parameters computed by the group.  Warps without a
 // pair in a round skip straight to the barrier (they would otherwise steal
 // issue slots from the latency-bound active warps).
-template <int LP, bool SMEM, int E>
+template <int LP, bool SMEM, int E, int NTH = 512>
 __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, double tiny2, double thr,
                              SvdSmem& S) {
   // SMEM: index the staged copy through S.cs so the compiler emits LDS/STS
   double* X = SMEM ? S.cs : Xg;
-  constexpr int GPW = 32 / LP;
+  constexpr int GPW = 32 / LP, NT = NTH, NW = NTH / 32;   // shadow the 512-thread defaults
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int grp = wid * GPW + lane / LP, gl = lane % LP;
   const int ngroups = NW * GPW;
@@ -276,8 +277,11 @@ __device__ int jacobi_groups(double* Xg, int ld, int m, int n, double tol, doubl
 }
 
 
+// NTH threads; cap: doubles of S.cs the launch allocated
+template <int NTH = 512>
 __device__ __noinline__ void svd_single(const hq_svd_prob& Pin, int* __restrict__ rank,
-                                        const double* __restrict__ scal, SvdSmem& S) {
+                                        const double* __restrict__ scal, SvdSmem& S, int cap = SMEM_DOUBLES) {
+  constexpr int NT = NTH, NW = NTH / 32;   // shadow the 512-thread defaults
   const hq_svd_prob P = Pin;
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int m = hq_dim(rank, P.m, P.m_ri);
@@ -292,7 +296,7 @@ __device__ __noinline__ void svd_single(const hq_svd_prob& Pin, int* __restrict_
     return;
   }
   const int lds = (m + 1) & ~1;  // even leading dim: 16 B aligned columns for double2
-  const bool staged = (size_t)lds * n <= SMEM_DOUBLES;
+  const bool staged = (size_t)lds * n <= (size_t)cap;
   double* X;
   int ld;
   if (staged) { X = S.cs; ld = lds; }
@@ -322,22 +326,22 @@ __device__ __noinline__ void svd_single(const hq_svd_prob& Pin, int* __restrict_
       // lane-group shape: as many lanes per pair as one pass of groups allows
       // (shorter per-pair dependency chains), enough rows per lane for m
       const int np0 = (n + 1) / 2;
-      if (np0 <= 16 || m > 256) {
-        if (m <= 128) nsweeps = jacobi_groups<32, true, 4>(X, ld, m, n, tol, tiny2, thr, S);
-        else if (m <= 256) nsweeps = jacobi_groups<32, true, 8>(X, ld, m, n, tol, tiny2, thr, S);
-        else nsweeps = jacobi_groups<32, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
-      } else if (np0 <= 32 || m > 128) {
-        if (m <= 128) nsweeps = jacobi_groups<16, true, 8>(X, ld, m, n, tol, tiny2, thr, S);
-        else nsweeps = jacobi_groups<16, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
+      if (np0 <= NW || m > 256) {
+        if (m <= 128) nsweeps = jacobi_groups<32, true, 4, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+        else if (m <= 256) nsweeps = jacobi_groups<32, true, 8, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+        else nsweeps = jacobi_groups<32, true, 16, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+      } else if (np0 <= 2 * NW || m > 128) {
+        if (m <= 128) nsweeps = jacobi_groups<16, true, 8, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+        else nsweeps = jacobi_groups<16, true, 16, NTH>(X, ld, m, n, tol, tiny2, thr, S);
       } else {
-        if (m <= 64) nsweeps = jacobi_groups<8, true, 8>(X, ld, m, n, tol, tiny2, thr, S);
-        else if (m <= 128) nsweeps = jacobi_groups<8, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
-        else nsweeps = jacobi_groups<16, true, 16>(X, ld, m, n, tol, tiny2, thr, S);
+        if (m <= 64) nsweeps = jacobi_groups<8, true, 8, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+        else if (m <= 128) nsweeps = jacobi_groups<8, true, 16, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+        else nsweeps = jacobi_groups<16, true, 16, NTH>(X, ld, m, n, tol, tiny2, thr, S);
       }
     } else {
-      if (m <= 128) nsweeps = jacobi_groups<8, false, 16>(X, ld, m, n, tol, tiny2, thr, S);
-      else if (m <= 256) nsweeps = jacobi_groups<16, false, 16>(X, ld, m, n, tol, tiny2, thr, S);
-      else nsweeps = jacobi_groups<32, false, 16>(X, ld, m, n, tol, tiny2, thr, S);
+      if (m <= 128) nsweeps = jacobi_groups<8, false, 16, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+      else if (m <= 256) nsweeps = jacobi_groups<16, false, 16, NTH>(X, ld, m, n, tol, tiny2, thr, S);
+      else nsweeps = jacobi_groups<32, false, 16, NTH>(X, ld, m, n, tol, tiny2, thr, S);
     }
   }
   for (int sweep = 0; sweep < MAX_SWEEPS && N > 0 && !(m <= 512); ++sweep) {
@@ -444,6 +448,17 @@ __device__ __noinline__ void svd_single(const hq_svd_prob& Pin, int* __restrict_
 #endif
   }
   (void)nsweeps;   // read by the HQ_DEBUG_SWEEPS build only
+}
+
+// Small cores, many per launch: 128-thread CTAs with only as much staging
+// memory as the launch's largest core needs, so several problems share an SM
+// (the round-robin rounds are latency chains; co-resident problems fill them).
+constexpr int SMALL_NT = 128;
+__global__ void __launch_bounds__(SMALL_NT) svd_small_kernel(const hq_svd_prob* __restrict__ probs,
+                                                             int* __restrict__ rank,
+                                                             const double* __restrict__ scal, int cap) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  svd_single<SMALL_NT>(probs[blockIdx.x], rank, scal, *reinterpret_cast<SvdSmem*>(smem_raw), cap);
 }
 
 __global__ void __launch_bounds__(NT, 1) svd_kernel(const hq_svd_prob* __restrict__ probs,

@@ -1084,6 +1084,22 @@ def qrcp_launch(nprob, m, n, sms=148):
     return 8, QRCP_SMEM_MAX, 512   # reduced in place in global memory
 
 
+SVD_SMALL_MAX = int(os.environ.get("HQ_SVD_SMALL_MAX", "8192"))   # doubles of staging per small-core CTA
+
+
+def svd_small_doubles(nprob, m, n, sms=148):
+    """Staging doubles for the small-core Jacobi kernel (128-thread CTAs,
+    several per SM), or 0 when the launch should not use it: it pays when a
+    launch has more problems than SMs (the cluster kernels would run in many
+    waves of one CTA per SM) and the cores are small enough for >= 2 CTAs to
+    share an SM (tools/svd_small_ab.py, 1482 cores: 48 x 32 9.1 -> 1.6 ms,
+    80 x 48 14.9 -> 7.5 ms, 112 x 64 26.4 -> 18.3 ms against 2-CTA clusters)."""
+    need = (m + 1) // 2 * 2 * n
+    if nprob > sms and m <= 128 and need <= SVD_SMALL_MAX:
+        return max(64, need)
+    return 0
+
+
 def svd_cluster_runtime(nprob, m, n, sms=148):
     """Cluster size for a Jacobi launch whose largest core is m x n (run-time
     sizes, e.g. from a previous run of the plan): the smallest cluster whose
@@ -1091,8 +1107,10 @@ def svd_cluster_runtime(nprob, m, n, sms=148):
     path is 4-6x slower), widened while the launch still fits one wave."""
     if n <= 0 or m <= 0:
         return 1
-    if _svd_fits(1, m, n) and (n + 1) // 2 <= SVD_SINGLE_MAX_PAIRS:
-        return 1
+    if svd_small_doubles(nprob, m, n, sms):
+        return 0
+    if _svd_fits(1, m, n) and ((n + 1) // 2 <= SVD_SINGLE_MAX_PAIRS or nprob > sms):
+        return 1   # few pairs, or more problems than SMs: one CTA each beats clusters in waves
     fit = [G for G in (2, 4, 8) if _svd_fits(G, m, n)]
     if not fit:
         # too wide for 8 CTAs: a (non-portable) 16-CTA cluster if it fits there
@@ -1131,15 +1149,17 @@ def retune_clusters(builder, rk, margin=1.1):
         m2 = min(int(mm * margin) + 1, p[5].cap) if mm else 0
         n2 = min(int(nn * margin) + 1, m2) if nn else 0
         G = svd_cluster_runtime(len(probs), m2, n2)
-        block = svd_use_block(len(probs), m2, n2, G)
+        block = svd_use_block(len(probs), m2, n2, G) if G else False
         bG = svd_block_cluster(len(probs), n2) if block else 1
+        small = svd_small_doubles(len(probs), m2, n2) if G == 0 else 0
         if block:
             G = 1
         if (G != extra.get("cluster", 1) or block != extra.get("block", False)
-                or bG != extra.get("bcluster", 1)):
+                or bG != extra.get("bcluster", 1) or small != extra.get("small", 0)):
             extra["cluster"] = G
             extra["block"] = block
             extra["bcluster"] = bG
+            extra["small"] = small
             changed += 1
     return changed
 
@@ -1500,7 +1520,8 @@ class CompiledPlan:
                 if ex.get("block"):
                     rc = lib.hq_svd_block(stream_handle, dp + o1, cnt, rk, sc, ex.get("bcluster", 1))
                 else:
-                    rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0))
+                    rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0),
+                                    ex.get("small", 0))
             elif kind == "applyq":
                 rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk, ex.get("max_cols", 0))
             elif kind == "leaf_gather":

@@ -226,15 +226,21 @@ def test_qr_and_applyq(dev, m, k, cl):
     assert np.abs(back(dX, m, c) - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
 
 
-@pytest.mark.parametrize("xform,CL", [(0, 1), (1, 1), (1, 2), (1, 4), (1, 8), (1, 16)])
+@pytest.mark.parametrize("xform,CL", [(0, 1), (1, 1), (1, 2), (1, 4), (1, 8), (1, 16), (0, 0), (1, 0)])
 @pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60),
                                       (200, 190, 120), (256, 256, 200), (130, 128, 128), (448, 448, 300),
-                                      (600, 300, 250), (640, 200, 150)])
+                                      (600, 300, 250), (640, 200, 150), (48, 32, 20), (112, 36, 30),
+                                      (128, 64, 50)])
 def test_svd_truncation(dev, m, n, keep, xform, CL):
     if xform == 0 and m >= 150:
         pytest.skip("unpreconditioned Jacobi is not used by the plan at this size")
     if CL == 16 and m < 256:
         pytest.skip("16-CTA clusters carry only the widest cores")
+    if CL == 0 and m > 256:
+        pytest.skip("the small-core kernel carries cores of at most 128 rows (larger ones only as a fallback)")
+    # CL = 0: the 128-thread small-core kernel; staging for cores of up to 4096
+    # doubles, larger ones take its global-memory path
+    SMALL = 4096
     # cluster launches pick one SM / the cluster / the global-memory path from
     # the run-time size, so every (size, cluster) combination must be exact
     MM = m
@@ -257,7 +263,7 @@ def test_svd_truncation(dev, m, n, keep, xform, CL):
     p = np.zeros(1, _abi.SVD_PROB)
     p[0] = (dC.data_ptr(), dU.data_ptr(), dW.data_ptr(), ldc, m, m, -1, n, -1, min(m, n), 0, 1, -1, thr, xform, 0)
     dp = put(torch, p)
-    assert lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), CL, MM) == 0
+    assert lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), CL, MM, SMALL) == 0
     torch.cuda.synchronize()
     k = int(rank[0].item())
     assert k == min(keep, len(s))
@@ -266,6 +272,60 @@ def test_svd_truncation(dev, m, n, keep, xform, CL):
     # projection error of C onto span(U) equals the dropped tail (<= thr)
     err = np.linalg.norm(C - U @ (U.T @ C), 2)
     assert err <= thr * 1.0001 + 1e-12 * np.linalg.norm(C, 2)
+
+
+@pytest.mark.parametrize("G,threads,smem", [(1, 256, None), (1, 512, None), (2, 512, None), (4, 256, None),
+                                             (8, 512, None), (2, 512, "hdr"), (1, 256, "hdr")])
+@pytest.mark.parametrize("m,n,keep", [(6, 6, 3), (25, 25, 25), (40, 13, 7), (13, 40, 9), (150, 150, 60),
+                                      (200, 190, 120), (208, 208, 112), (97, 33, 30), (17, 17, 1),
+                                      (300, 280, 150)])
+def test_qrcp_then_svd(dev, m, n, keep, G, threads, smem):
+    """hq_qrcp (pivoted R of the core, stopped at 1e-3 thr) followed by the
+    xform-2 Jacobi on its rows: rank, orthogonality and projection error as
+    for the unpivoted path; every cluster size, both thread counts, and the
+    in-place global-memory mode (shared memory holds only the norms and the
+    candidate buffers, which the caller must always provide)."""
+    from paper_1809_10585_b200.plan import QRCP_SMEM_MAX, qrcp_smem
+    torch, lib = dev
+    rng = np.random.default_rng(m * n + 1)
+    kk = min(m, n)
+    u = np.linalg.qr(rng.standard_normal((m, kk)))[0]
+    v = np.linalg.qr(rng.standard_normal((n, kk)))[0]
+    s = np.logspace(0, -14, kk)
+    C = (u * s) @ v.T                      # m x n; left singular vectors wanted
+    thr = float(np.sqrt(s[keep - 1] * s[keep])) if keep < len(s) else 0.0
+    # the pivoted QR works on C^T (n x m): its R rows transposed are X (m x r)
+    dC = colmajor(torch, C.T.copy())
+    need = qrcp_smem(G, n, m, threads)
+    sm = need or QRCP_SMEM_MAX
+    if smem == "hdr":   # room for the norms and candidates only: the slice stays in global memory
+        sm = 8 + 2 * -(-m // G) + 2 * G * (((n + 1) & ~1) + 4) + 8
+    dW = torch.zeros(((m + 1) // 2 * 2) * kk, dtype=torch.float64, device="cuda")
+    dU = torch.zeros(m * kk, dtype=torch.float64, device="cuda")
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    scal = torch.zeros(2, dtype=torch.float64, device="cuda")
+    q = np.zeros(1, _abi.QRCP_PROB)
+    q[0] = (dC.data_ptr(), n, n, -1, m, -1, 2, -1, 0, 1e-3 * thr)
+    dq = put(torch, q)
+    assert lib.hq_qrcp(None, dq.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), G, sm, threads) == 0
+    torch.cuda.synchronize()
+    r = int(rank[2].item())
+    assert min(keep, kk) <= r <= kk
+    p = np.zeros(1, _abi.SVD_PROB)
+    p[0] = (dC.data_ptr(), dU.data_ptr(), dW.data_ptr(), n, m, m, -1, kk, 2, kk, 0, 1, -1, thr, 2, 0)
+    dp = put(torch, p)
+    assert lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), 1, m, 0) == 0
+    torch.cuda.synchronize()
+    k = int(rank[0].item())
+    assert k == min(keep, kk)
+    U = back(dU, m, kk)[:, :k]
+    assert np.linalg.norm(U.T @ U - np.eye(k)) <= 1e-12 * max(k, 1)
+    err = np.linalg.norm(C - U @ (U.T @ C), 2)
+    assert err <= thr * 1.001 + 1e-12 * np.linalg.norm(C, 2)
+    # the rows kept are R of a pivoted QR: singular values of C up to the dropped block
+    Rk = back(dC, n, m)[:r, :]
+    sv = np.linalg.svd(Rk, compute_uv=False)
+    assert np.abs(sv[:k] - s[:k]).max() <= 2e-3 * max(thr, 1e-13) + 1e-13
 
 
 @pytest.mark.parametrize("xform,G", [(0, 1), (1, 1), (1, 2), (1, 4), (1, 8)])

@@ -122,4 +122,4 @@ def test_retune_clusters_uses_the_rank_table():
         elif kind != "svd":
             assert ex == old
         else:
-            assert ex["cluster"] in (1, 2, 4, 8)
+            assert ex["cluster"] in (0, 1, 2, 4, 8)

@@ -37,7 +37,7 @@ for n in sizes:
     dp = put(p)
     res = {}
     G = svd_cluster_runtime(P, n, n)
-    for name, fn in (("scalar G=%d" % G, lambda: lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), G, n)),
+    for name, fn in (("scalar G=%d" % G, lambda: lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), G, n, 0)),
                      ("block", lambda: lib.hq_svd_block(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), svd_block_cluster(P, n)))):
         fn(); torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

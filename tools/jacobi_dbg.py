@@ -40,7 +40,7 @@ for n in sizes:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         if name == "scalar":
-            lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), 1, n)
+            lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), 1, n, 0)
         else:
             lib.hq_svd_block(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), svd_block_cluster(1, n))
         e1.record(); torch.cuda.synchronize()

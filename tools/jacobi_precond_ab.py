@@ -38,7 +38,7 @@ def run(X, thr):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        assert lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), G, m) == 0
+        assert lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), G, m, 0) == 0
         e1.record(); torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     k = int(rank[2].item())

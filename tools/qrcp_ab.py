@@ -63,7 +63,7 @@ for C, thr in cores:
         else:
             nn = min(k1, k2)
         Gs = svd_cluster_runtime(P, k1, nn)
-        ts = timed(lambda: lib.hq_svd(None, dsp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), Gs, k1),
+        ts = timed(lambda: lib.hq_svd(None, dsp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), Gs, k1, 0),
                    (lambda: None) if mode == "piv" else (lambda: dC.copy_(src)))
         k = int(rank[2].item())
         kall = rank[2:2 + P].cpu().numpy()

@@ -30,7 +30,7 @@ for n in ns:
                     dC[i].copy_(torch.tensor(M.T.copy(), device="cuda"))
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(); rc = lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), CL, n); e1.record()
+                e0.record(); rc = lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), CL, n, 0); e1.record()
                 torch.cuda.synchronize()
                 best = min(best, e0.elapsed_time(e1))
             res.append(f"CL{CL} {best:7.3f} ms (rc {rc}, rank {int(rank[0])})")

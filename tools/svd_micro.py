@@ -24,7 +24,7 @@ for n, kind in cases:
             p = np.zeros(1, _abi.SVD_PROB); p[0] = (dC.data_ptr(), dU.data_ptr(), dW.data_ptr(), n, n, n, -1, n, -1, n, 0, 1, -1, 1e-10, xf, 0)
             dp = put(p); torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(); lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), CL, MM); e1.record(); torch.cuda.synchronize()
+            e0.record(); lib.hq_svd(None, dp.data_ptr(), 1, rank.data_ptr(), scal.data_ptr(), CL, MM, 0); e1.record(); torch.cuda.synchronize()
         k = int(rank[0]); U = dU.cpu().numpy().reshape(n, n).T[:, :k]
         err = np.linalg.norm(C - U @ (U.T @ C), 2)
         print(n, kind, "xform", xf, "cluster", CL, "ms %.3f" % e0.elapsed_time(e1), "rank", k, "sweeps(dbg)", int(rank[2]), "cyc/16 norm,intra,inter,xchg", rank[3:7].tolist(), "round work/bar", rank[7:9].tolist(), "proj err %.2e" % err, "orth %.1e" % np.abs(U.T @ U - np.eye(k)).max())

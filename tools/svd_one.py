@@ -22,6 +22,6 @@ dp = torch.tensor(np.frombuffer(p.tobytes(), np.uint8), device="cuda")
 torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-rc = lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), CL, n)
+rc = lib.hq_svd(None, dp.data_ptr(), P, rank.data_ptr(), scal.data_ptr(), CL, n, 0)
 e1.record(); torch.cuda.synchronize()
 print(f"n={n} CL={CL} nprob={P}: {e0.elapsed_time(e1):.3f} ms rc={rc} rank={int(rank[0])}")
