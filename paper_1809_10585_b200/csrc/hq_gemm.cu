@@ -578,10 +578,24 @@ __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __res
   if (skip && *skip) return;
   constexpr int RQ = 4;
   const int bid = blockIdx.x;
+  // last problem with item0 <= bid: 32-ary search by every warp (3 dependent
+  // loads for 32768 problems instead of 15 for the binary search -- the
+  // descriptor fetches were most of a CTA's life on ~50 KB work items)
   int lo = 0, hi = nprob - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (probs[mid].item0 <= bid) lo = mid; else hi = mid - 1;
+  {
+    const int ln = threadIdx.x & 31;
+    while (lo < hi) {
+      const int span = hi - lo;                 // candidates lo+1 .. hi
+      const int step = (span + 31) / 32;        // probe lo + step * (ln + 1), clamped
+      const int idx = min(lo + step * (ln + 1), hi);
+      const bool le = probs[idx].item0 <= bid;
+      const unsigned bal = __ballot_sync(0xffffffffu, le);
+      const int cnt = __popc(bal);              // probes are monotone: the first cnt are <= bid
+      const int nlo = cnt == 0 ? lo : min(lo + step * cnt, hi);
+      const int nhi = cnt == 32 ? hi : min(lo + step * (cnt + 1), hi) - 1;
+      lo = nlo;
+      hi = max(nhi, nlo);
+    }
   }
   const hq_gemm_prob P = probs[lo];
   const int ks = (lo + 1 < nprob ? probs[lo + 1].item0 : nitems) - P.item0;

@@ -39,6 +39,7 @@ NB = 16          # QR panel width (hq_qr.cu)
 TALL_ROWS = 1024  # factor stacks taller than this are QR'd by one-level TSQR
 TSQR_CH = 512     # TSQR chunk rows (register-cached panels)
 GEMM_TILE = 64   # GEMM output tile (hq_gemm.cu)
+FLAT_ITEM_K = int(os.environ.get("HQ_FLAT_ITEM_K", "2048"))   # K rows per work item of the one-launch V^T X kernel
 SKINNY_MAX_COLS = 4  # hq_gemm_skinny: outputs with at most this many columns
 SVD_MAX_N = 1024
 
@@ -344,7 +345,8 @@ class Builder:
         extra["lane"] = self.lane
         extra["level"] = self.cur_level
         if kind == "qr" and "cluster" not in extra:
-            extra["cluster"] = qr_cluster(probs)
+            force = os.environ.get("HQ_QR_CLUSTER_" + str(extra.get("role", "")).upper())
+            extra["cluster"] = int(force) if force else qr_cluster(probs)
         if self.track:
             # the live allocation instances this op touches, resolved now
             # (scratch regions are reused later): the units distributed.py
@@ -486,7 +488,7 @@ class Builder:
             nc = 2 if ncap <= 2 else 4
             for prob in p1:
                 items.append(tot)
-                it = max(1, min(32, sum(t[8].cap for t in prob[5]) // 512))
+                it = max(1, min(32, sum(t[8].cap for t in prob[5]) // FLAT_ITEM_K))
                 tot += it
                 slots.append((1, it, prob[2].cap * nc))
             ex = dict(tiles=1, ksplit=tot, skip=skip, skinny=True, ncmax=ncap, mode=5,

@@ -10,10 +10,13 @@ from paper_1809_10585_b200.hqr import HQREngine
 from paper_1809_10585_b200.plan import _dv
 ci = int(sys.argv[1]); n = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] != "0" else None
 B = int(sys.argv[3]) if len(sys.argv) > 3 else 1
-kcap = int(sys.argv[4]) if len(sys.argv) > 4 else (192 if B > 1 else 512)
+kcap = (192 if B > 1 else 512) if len(sys.argv) <= 4 else (sys.argv[4] if sys.argv[4] == "profile" else int(sys.argv[4]))
 out = sys.argv[5] if len(sys.argv) > 5 else "gpurun_out/op_times.tsv"
 c = gen.CONFIGS[ci]
 mats = [gen.gen_config(ci, seed=s, n=n) for s in range(B)]
+if kcap == "profile":
+    import bench
+    kcap = bench.kcap_profile(c, mats[0].tree())
 eng = HQREngine(mats[0].tree(), B, c["tol"], kcap=kcap, use_graph=False, stream_out=B > 1)
 eng.factorize(mats)
 eng.factorize(mats)
