@@ -66,6 +66,18 @@ HQ_DEV double hq_mask(double v, int r, int c, int mask) {
 
 static inline int hq_err(cudaError_t e) { return (int)e; }
 
+// Explicit shared-memory accesses for pointers the compiler only knows as
+// generic (struct references passed into non-inlined functions): a generic
+// LD/ST to shared memory resolves the address space at run time and waits on
+// the long scoreboard; LDS/STS do not.
+HQ_DEV unsigned hq_smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+HQ_DEV double hq_lds(unsigned a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+HQ_DEV void hq_sts(unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory"); }
+
 // Deterministic K-split: every slice of an output block has stored its
 // partial sum into its own workspace slot; the CTA whose arrival completes
 // the block's counter (a device int, zero between uses) returns true, resets
@@ -99,6 +111,12 @@ HQ_DEV void dmma884(double& d0, double& d1, double a, double b) {
 HQ_DEV void cp_async8(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+// 16-byte variant (both addresses 16-byte aligned); .cg: the data is used
+// from shared memory only, no L1 allocation
+HQ_DEV void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
 }
 HQ_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
@@ -154,5 +172,32 @@ HQ_DEV Refl make_refl(double x0, double ss, double sc, double isc) {
     r.inv = sc * iu;                           // y = v * inv
     r.gamma = 2.0 / (1.0 + ss * iu * iu);
   }
+  return r;
+}
+
+// Reflector of x = [x0; v] from ss = sum v^2 (both in the safe range, see
+// refl_safe) with the hardware reciprocal / reciprocal square root refined
+// by Newton steps to full FP64 accuracy: ||x||, 1 / u1 and gamma = |u1| /
+// ||x|| (= 2 / (1 + ss / u1^2)) cost two short dependent chains instead of a
+// software sqrt and two divisions on the per-step critical path.
+HQ_DEV Refl make_refl_fast(double x0, double ss) {
+  const double tot = fma(x0, x0, ss);
+  double rn;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(tot));
+  const double ht = 0.5 * tot;
+  rn = rn * fma(-ht * rn, rn, 1.5);
+  rn = rn * fma(-ht * rn, rn, 1.5);
+  double nrm = tot * rn;
+  nrm = fma(0.5 * rn, fma(-nrm, nrm, tot), nrm);
+  const double sg = x0 < 0.0 ? -1.0 : 1.0;
+  const double u1 = fma(sg, nrm, x0);
+  double iu;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(iu) : "d"(u1));
+  iu = iu * fma(-u1, iu, 2.0);
+  iu = iu * fma(-u1, iu, 2.0);
+  Refl r;
+  r.rho = -sg * nrm;
+  r.inv = iu;
+  r.gamma = fabs(u1) * rn;
   return r;
 }

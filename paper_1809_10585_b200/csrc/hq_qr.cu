@@ -58,20 +58,24 @@ struct QrSmem {
 // column j's reflector, formed by the warp that caches column j in `c`
 // (the diagonal entry x0 comes from its owning lane with one shuffle)
 template <int E>
-__device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int lane, double* ybuf,
+__device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int lane, unsigned ybuf,
                                            double* tau, QrSmem& S) {
-  double ss = 0.0, x0 = 0.0;
+  // four partial sums: the FP64 FMA chain of one accumulator would be the
+  // longest dependency of the column step
+  double sp[4] = {0.0, 0.0, 0.0, 0.0}, x0 = 0.0;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = lane + 32 * e;
     const double v = c[e];
-    if (i > j && i < rows) ss = fma(v, v, ss);
+    if (i > j && i < rows) sp[e & 3] = fma(v, v, sp[e & 3]);
     if (e == (j >> 5)) x0 = v;
   }
+  double ss = (sp[0] + sp[1]) + (sp[2] + sp[3]);
   x0 = __shfl_sync(0xffffffffu, x0, j & 31);
   ss = warp_sum(ss);
   double sc = 1.0, isc = 1.0;
-  if (!refl_safe(x0, ss)) {   // warp-uniform, rare: rescale by max|x|
+  const bool safe = refl_safe(x0, ss);
+  if (!safe) {   // warp-uniform, rare: rescale by max|x|
     double amax = 0.0;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
@@ -91,14 +95,17 @@ __device__ __forceinline__ void own_column(double (&c)[E], int j, int rows, int 
     }
     ss = warp_sum(ss);
   }
-  const Refl R = make_refl(x0, ss, sc, isc);
+  // common case (no rescaling): norm, 1 / u1 and gamma from the hardware
+  // rsqrt / rcp refined by Newton steps instead of a software sqrt and two
+  // divisions on the column step's critical path
+  const Refl R = safe ? make_refl_fast(x0, ss) : make_refl(x0, ss, sc, isc);
   const double gamma = R.gamma, rho = R.rho, inv = R.inv;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int i = lane + 32 * e;
     if (i > j && i < rows) c[e] *= inv;
     if (i == j) c[e] = rho;
-    ybuf[i] = i > j ? c[e] : (i == j ? 1.0 : 0.0);
+    hq_sts(ybuf + 8u * i, i > j ? c[e] : (i == j ? 1.0 : 0.0));
   }
   if (lane == 0) { S.dv[j] = gamma; tau[j] = gamma; }
 }
@@ -122,28 +129,34 @@ __device__ __noinline__ void panel_factor_reg(double* P, int ldp, int rows, int 
       col[q][e] = (c < pw && i < rows) ? P[i + (size_t)c * ldp] : 0.0;
     }
   }
+  const unsigned wsp_a = hq_smem_addr(S.wsp), bcast_a = hq_smem_addr(S.bcast), dv_a = hq_smem_addr(S.dv);
   for (int j = 0; j < pw; ++j) {
-    double* ybuf = (j & 1) ? S.wsp : S.bcast;  // y_j broadcast (rows <= 32 E)
+    // y_j broadcast (rows <= 32 E), as a shared-space address: LDS / STS
+    const unsigned ybuf = (j & 1) ? wsp_a : bcast_a;
     if (wid == (j % NW)) {
       if (j < NW) own_column<E>(col[0], j, rows, lane, ybuf, tau, S);
       else own_column<E>(col[1], j, rows, lane, ybuf, tau, S);
     }
     __syncthreads();
-    const double gamma = S.dv[j];
-    double y[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) y[e] = ybuf[lane + 32 * e];
+    const double gamma = hq_lds(dv_a + 8u * j);
+    // the tallest panels (E = 32) re-read y_j for the update instead of keeping it:
+    // 2 E column values + E of y would exceed the register file and spill
+    constexpr bool KEEPY = E <= 24;
+    constexpr int EY = KEEPY ? E : 1;
+    double y[EY];
     // both cached columns: dots first, then the two reductions interleaved
     double d[2];
+    {
+      double dp[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
 #pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; e += 2) {
-        d0 = fma(y[e], col[q][e], d0);
-        if (e + 1 < E) d1 = fma(y[e + 1], col[q][e + 1], d1);
+      for (int e = 0; e < E; ++e) {
+        const double ye = hq_lds(ybuf + 8u * (lane + 32 * e));
+        if (KEEPY) y[e] = ye;
+        dp[0][e & 3] = fma(ye, col[0][e], dp[0][e & 3]);
+        dp[1][e & 3] = fma(ye, col[1][e], dp[1][e & 3]);
       }
-      d[q] = d0 + d1;
+      d[0] = (dp[0][0] + dp[0][1]) + (dp[0][2] + dp[0][3]);
+      d[1] = (dp[1][0] + dp[1][1]) + (dp[1][2] + dp[1][3]);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -157,7 +170,8 @@ __device__ __noinline__ void panel_factor_reg(double* P, int ldp, int rows, int 
       if (c > j) {
         const double gd = gamma * d[q];
 #pragma unroll
-        for (int e = 0; e < E; ++e) col[q][e] = fma(-gd, y[e], col[q][e]);
+        for (int e = 0; e < E; ++e)
+          col[q][e] = fma(-gd, KEEPY ? y[e] : hq_lds(ybuf + 8u * (lane + 32 * e)), col[q][e]);
       } else if (lane == 0) {
         S.dmat[c * NB + j] = d[q];   // y_c^T y_j  (c < j)
       }
@@ -276,12 +290,31 @@ __device__ __forceinline__ double yval(const double* P, int ldp, int i, int a) {
   const double v = P[i + (size_t)a * ldp];
   return i > a ? v : (i == a ? 1.0 : 0.0);
 }
+// the same from a shared-space address (LDS instead of a generic load)
+__device__ __forceinline__ double yval_s(unsigned pa, int ldp, int i, int a) {
+  const double v = hq_lds(pa + 8u * (unsigned)(i + a * ldp));
+  return i > a ? v : (i == a ? 1.0 : 0.0);
+}
 
 // stage cols columns of rows rows (global, ld lds) into shared dst (ld ldd)
 // with asynchronous copies; ends with a barrier
 __device__ __forceinline__ void stage_cols(double* dst, int ldd, const double* src, int lds, int rows, int cols) {
-  for (int c = 0; c < cols; ++c)
-    for (int i = threadIdx.x; i < rows; i += NT) cp_async8(dst + i + (size_t)c * ldd, src + i + (size_t)c * lds);
+  // 16-byte copies when every column start is 16-byte aligned on both sides
+  // (ldd is a multiple of 4 by construction): half the copy instructions
+  const bool vec = ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) && ((lds | ldd) & 1) == 0;
+  if (vec) {
+    const int pairs = rows >> 1;
+    for (int e = threadIdx.x; e < pairs * cols; e += NT) {
+      const int c = e / pairs, i = 2 * (e - c * pairs);
+      cp_async16(dst + i + (size_t)c * ldd, src + i + (size_t)c * lds);
+    }
+    if (rows & 1)
+      for (int c = threadIdx.x; c < cols; c += NT)
+        cp_async8(dst + rows - 1 + (size_t)c * ldd, src + rows - 1 + (size_t)c * lds);
+  } else {
+    for (int c = 0; c < cols; ++c)
+      for (int i = threadIdx.x; i < rows; i += NT) cp_async8(dst + i + (size_t)c * ldd, src + i + (size_t)c * lds);
+  }
   cp_async_wait_all();
   __syncthreads();
 }
@@ -294,11 +327,15 @@ __device__ __forceinline__ void stage_cols(double* dst, int ldd, const double* s
 // buffer xs (xs_cap doubles) is given, each chunk is first staged into shared
 // memory with asynchronous copies (one round trip to L2 instead of one per
 // k-block); the result goes back to X.
-template <class SM>
-__device__ __noinline__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, const double* tp,
-                                              double* X, int ldx, int ncols, bool trans_t, SM& S,
-                                              double* xs = nullptr, int xs_cap = 0) {
+// YSH: Y lives in shared memory, XSH: the chunk of X is read from shared
+// memory (staged, or X itself) -- then both are fetched with LDS.
+template <bool YSH, bool XSH, class SM>
+__device__ __noinline__ void apply_panel_cols_impl(const double* Y, int ldy, int rows, int pw, const double* tp,
+                                                   double* X, int ldx, int ncols, bool trans_t, SM& S,
+                                                   double* xs, int xs_cap) {
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const unsigned ya = YSH ? hq_smem_addr(Y) : 0u;
+  auto yv = [&](int i, int a) { return YSH ? yval_s(ya, ldy, i, a) : yval(Y, ldy, i, a); };
   const int gq = lane >> 2, tq = lane & 3;
   int cwmax = CW;
   const int ldxs = pad_ld(rows);
@@ -331,6 +368,7 @@ __device__ __noinline__ void apply_panel_cols(const double* Y, int ldy, int rows
       double e00 = 0.0, e01 = 0.0, e10 = 0.0, e11 = 0.0;
       const int j = nt * 8 + gq;          // B col  (chunk column)
       const double* xc = Xr + (size_t)(j < cw ? j : 0) * ldr;
+      const unsigned xca = XSH ? hq_smem_addr(xc) : 0u;
       const int kb = kp * kchunk, ke = min(rows, kb + kchunk);
       for (int k0 = kb; k0 < ke; k0 += 32) {
         double a0[8], a1[8], bv[8];
@@ -338,9 +376,9 @@ __device__ __noinline__ void apply_panel_cols(const double* Y, int ldy, int rows
         for (int u = 0; u < 8; ++u) {
           const int ia = k0 + 4 * u + tq;
           const bool in = ia < ke;
-          a0[u] = (in && gq < pw) ? yval(Y, ldy, ia, gq) : 0.0;
-          a1[u] = (in && 8 + gq < pw) ? yval(Y, ldy, ia, 8 + gq) : 0.0;
-          bv[u] = (in && j < cw) ? xc[ia] : 0.0;
+          a0[u] = (in && gq < pw) ? yv(ia, gq) : 0.0;
+          a1[u] = (in && 8 + gq < pw) ? yv(ia, 8 + gq) : 0.0;
+          bv[u] = (in && j < cw) ? (XSH ? hq_lds(xca + 8u * ia) : xc[ia]) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; u += 2) {
@@ -408,15 +446,22 @@ __device__ __noinline__ void apply_panel_cols(const double* Y, int ldy, int rows
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int a = 4 * q + tq;
-        av[q] = (i < rows && a < pw) ? -yval(Y, ldy, i, a) : 0.0;
+        av[q] = (i < rows && a < pw) ? -yv(i, a) : 0.0;
       }
 #pragma unroll
       for (int nt = 0; nt < CW / 8; ++nt) {
         if (nt >= ntn) break;
         const int j = nt * 8 + 2 * tq;
         const double* x0 = Xr + (size_t)j * ldr;
-        double d0 = (i < rows && j < cw) ? x0[i] : 0.0;
-        double d1 = (i < rows && j + 1 < cw) ? x0[ldr + i] : 0.0;
+        double d0, d1;
+        if (XSH) {
+          const unsigned x0a = hq_smem_addr(x0);
+          d0 = (i < rows && j < cw) ? hq_lds(x0a + 8u * i) : 0.0;
+          d1 = (i < rows && j + 1 < cw) ? hq_lds(x0a + 8u * (ldr + i)) : 0.0;
+        } else {
+          d0 = (i < rows && j < cw) ? x0[i] : 0.0;
+          d1 = (i < rows && j + 1 < cw) ? x0[ldr + i] : 0.0;
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) dmma884(d0, d1, av[q], bw[nt][q]);
         double* xo = Xw + (size_t)j * ldx;
@@ -426,6 +471,21 @@ __device__ __noinline__ void apply_panel_cols(const double* Y, int ldy, int rows
     }
     __syncthreads();
     HQ_TMARK(2);
+  }
+}
+
+template <class SM>
+__device__ __forceinline__ void apply_panel_cols(const double* Y, int ldy, int rows, int pw, const double* tp,
+                                                 double* X, int ldx, int ncols, bool trans_t, SM& S,
+                                                 double* xs = nullptr, int xs_cap = 0) {
+  if (xs && (min(CW, (xs_cap / pad_ld(rows)) & ~7) < 8)) xs = nullptr;   // the impl's own test
+  const bool ysh = __isShared(Y) != 0, xsh = xs != nullptr || __isShared(X) != 0;   // block-uniform
+  if (ysh) {
+    if (xsh) apply_panel_cols_impl<true, true>(Y, ldy, rows, pw, tp, X, ldx, ncols, trans_t, S, xs, xs_cap);
+    else apply_panel_cols_impl<true, false>(Y, ldy, rows, pw, tp, X, ldx, ncols, trans_t, S, xs, xs_cap);
+  } else {
+    if (xsh) apply_panel_cols_impl<false, true>(Y, ldy, rows, pw, tp, X, ldx, ncols, trans_t, S, xs, xs_cap);
+    else apply_panel_cols_impl<false, false>(Y, ldy, rows, pw, tp, X, ldx, ncols, trans_t, S, xs, xs_cap);
   }
 }
 
@@ -621,9 +681,15 @@ __device__ void factor_panel_step(const hq_qr_prob& Q, double* W, int ld, int m,
   }
   factor_panel_core(Q, P, ldp, rows, pw, p0, S);
   // trailing columns: A_trail := Q_p^T A_trail
-  if (do_trailing && p0 + pw < k)
+  // (X chunks are staged in S.ybuf; a staged panel shorter than STAGE_ROWS
+  // leaves the tail of S.panel free, which is contiguous with S.ybuf: wider
+  // chunks, fewer passes over Y)
+  if (do_trailing && p0 + pw < k) {
+    double* xs = staged ? S.panel + (size_t)ldp * NB : S.ybuf;
+    const int xs_cap = staged ? (STAGE_ROWS + 4) * NB - ldp * NB + YBUF : YBUF;
     apply_panel_cols(P, ldp, rows, pw, S.tp, W + p0 + (size_t)(p0 + pw) * ld, ld, k - p0 - pw, true, S,
-                     S.ybuf, YBUF);
+                     xs, xs_cap);
+  }
   __syncthreads();
   if (do_merge) merge_T(Q, W, ld, m, r, p0, P, ldp, S.tp, S);
   if (staged)

@@ -44,33 +44,6 @@ __device__ __forceinline__ double* cp_remote(double* p, int r) {
   else return p;
 }
 
-// Reflector of x = [x0; v] from ss = sum v^2 (both in the safe range, see
-// refl_safe) with the hardware reciprocal / reciprocal square root refined
-// by Newton steps to full FP64 accuracy: ||x||, 1 / u1 and gamma = |u1| /
-// ||x|| (= 2 / (1 + ss / u1^2)) cost two short dependent chains instead of a
-// software sqrt and two divisions on the per-step critical path.
-HQ_DEV Refl cp_refl_fast(double x0, double ss) {
-  const double tot = fma(x0, x0, ss);
-  double rn;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rn) : "d"(tot));
-  const double ht = 0.5 * tot;
-  rn = rn * fma(-ht * rn, rn, 1.5);
-  rn = rn * fma(-ht * rn, rn, 1.5);
-  double nrm = tot * rn;
-  nrm = fma(0.5 * rn, fma(-nrm, nrm, tot), nrm);
-  const double sg = x0 < 0.0 ? -1.0 : 1.0;
-  const double u1 = fma(sg, nrm, x0);
-  double iu;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(iu) : "d"(u1));
-  iu = iu * fma(-u1, iu, 2.0);
-  iu = iu * fma(-u1, iu, 2.0);
-  Refl r;
-  r.rho = -sg * nrm;
-  r.inv = iu;
-  r.gamma = fabs(u1) * rn;
-  return r;
-}
-
 // pivot key of a column: its squared norm's bit pattern (monotonic for
 // non-negative doubles) with the low 11 bits replaced by 2047 - local column
 // (a CTA owns at most 2047 columns): one 64-bit maximum picks the largest norm
@@ -167,7 +140,7 @@ __global__ void qrcp_kernel(const hq_qrcp_prob* __restrict__ probs, int* __restr
         x0 = __shfl_sync(0xffffffffu, x0, 0);
         Refl R;
         if (refl_safe(x0, ss)) {
-          R = cp_refl_fast(x0, ss);
+          R = make_refl_fast(x0, ss);
         } else {   // warp-uniform, rare: rescale by max|x| (zero, tiny or huge columns)
           double amax = 0.0;
           __syncwarp();

@@ -407,7 +407,11 @@ class HQREngine(PlanIO):
         self.n_out = 0
         self.use_graph = use_graph
         self.graph = None
-        self.stream = torch.cuda.Stream(device=self.device)
+        # the chain lane outranks the side lanes: when both have CTAs pending
+        # the critical path gets the SMs first (priorities are recorded in
+        # the captured graph's kernel nodes)
+        prio = -1 if os.environ.get("HQB200_CHAIN_PRIORITY", "1") not in ("0", "") else 0
+        self.stream = torch.cuda.Stream(device=self.device, priority=prio)
         self.copy_stream = torch.cuda.Stream(device=self.device)
         self.h2d_stream = torch.cuda.Stream(device=self.device)
         self.side = [torch.cuda.Stream(device=self.device) for _ in range(self.plan.n_lanes - 1)]
