@@ -303,10 +303,12 @@ __device__ __forceinline__ void stage_cols(double* dst, int ldd, const double* s
   // (ldd is a multiple of 4 by construction): half the copy instructions
   const bool vec = ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) && ((lds | ldd) & 1) == 0;
   if (vec) {
-    const int pairs = rows >> 1;
-    for (int e = threadIdx.x; e < pairs * cols; e += NT) {
-      const int c = e / pairs, i = 2 * (e - c * pairs);
-      cp_async16(dst + i + (size_t)c * ldd, src + i + (size_t)c * lds);
+    // warp w copies columns w, w + NW, ...; lanes along the rows (no divisions)
+    const int pairs = rows >> 1, lane = threadIdx.x & 31;
+    for (int c = threadIdx.x >> 5; c < cols; c += NW) {
+      const double* sc = src + (size_t)c * lds;
+      double* dc = dst + (size_t)c * ldd;
+      for (int pi = lane; pi < pairs; pi += 32) cp_async16(dc + 2 * pi, sc + 2 * pi);
     }
     if (rows & 1)
       for (int c = threadIdx.x; c < cols; c += NT)
