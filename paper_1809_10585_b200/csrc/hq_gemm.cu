@@ -18,6 +18,12 @@ __device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bo
   const int sz = valid ? 8 : 0;
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz) : "memory");
 }
+// 16-byte copy of which the first `bytes` (0, 8 or 16) come from global
+// memory, the rest zero; both addresses 16-byte aligned
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -92,56 +98,93 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
     ti = 0; k0 = -BK; gk = -1;
     advance(ti, k0, gk);
   }
+  // element e of this thread's share of a staged k-tile -> (row/col, k).
+  // Operands whose rows are contiguous in memory (A with ta = 0, B with
+  // tb = 1) and 16-byte aligned are copied in pairs (elements 2p, 2p + 1 by
+  // the same thread: one 16-byte cp.async), the others one by one.
+  auto a_elem = [&](int e, bool vec, int ta, int& ii, int& kk) {
+    if (vec) { const int p = t + (e >> 1) * NTH; ii = 2 * (p % (BM / 2)) + (e & 1); kk = p / (BM / 2); }
+    else if (ta == 0) { const int idx = t + e * NTH; ii = idx % BM; kk = idx / BM; }
+    else { const int idx = t + e * NTH; kk = idx % BK; ii = idx / BK; }
+  };
+  auto b_elem = [&](int e, bool vec, int tb, int& jj, int& kk) {
+    if (vec) { const int p = t + (e >> 1) * NTH; jj = 2 * (p % (BN / 2)) + (e & 1); kk = p / (BN / 2); }
+    else if (tb == 0) { const int idx = t + e * NTH; kk = idx % BK; jj = idx / BK; }
+    else { const int idx = t + e * NTH; jj = idx % BN; kk = idx / BN; }
+  };
+  auto vec_a = [&](const hq_gemm_term& T) {
+    return T.ta == 0 && (((uintptr_t)T.a & 15) == 0) && (T.lda & 1) == 0;
+  };
+  auto vec_b = [&](const hq_gemm_term& T) {
+    return T.tb != 0 && (((uintptr_t)T.b & 15) == 0) && (T.ldb & 1) == 0;
+  };
   auto stage = [&](int buf, int ti_, int k0_) {
     const hq_gemm_term T = terms[P.term0 + ti_];
     const int kd = hq_dim(rank, T.k, T.k_ri);
+    const bool va = vec_a(T), vb = vec_b(T);
+    if (va) {
 #pragma unroll
-    for (int e = 0; e < EA; ++e) {
-      const int idx = t + e * NTH;
-      int ii, kk;
-      if (T.ta == 0) { ii = idx % BM; kk = idx / BM; }
-      else { kk = idx % BK; ii = idx / BK; }
-      const int gi = i0 + ii, gkk = k0_ + kk;
-      const bool ok = gi < m && gkk < kd;
-      const double* src = T.ta == 0 ? T.a + (ok ? gi + (size_t)gkk * T.lda : 0)
-                                    : T.a + (ok ? gkk + (size_t)gi * T.lda : 0);
-      cp_async8_zfill(&As[buf][kk][ii], src, ok);
+      for (int e = 0; e < EA; e += 2) {
+        int ii, kk;
+        a_elem(e, true, 0, ii, kk);
+        const int gi = i0 + ii, gkk = k0_ + kk;
+        const int nv = gkk < kd ? min(max(m - gi, 0), 2) : 0;
+        cp_async16_zfill(&As[buf][kk][ii], T.a + (nv ? gi + (size_t)gkk * T.lda : 0), 8 * nv);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < EA; ++e) {
+        int ii, kk;
+        a_elem(e, false, T.ta, ii, kk);
+        const int gi = i0 + ii, gkk = k0_ + kk;
+        const bool ok = gi < m && gkk < kd;
+        const double* src = T.ta == 0 ? T.a + (ok ? gi + (size_t)gkk * T.lda : 0)
+                                      : T.a + (ok ? gkk + (size_t)gi * T.lda : 0);
+        cp_async8_zfill(&As[buf][kk][ii], src, ok);
+      }
     }
+    if (vb) {
 #pragma unroll
-    for (int e = 0; e < EB; ++e) {
-      const int idx = t + e * NTH;
-      int jj, kk;
-      if (T.tb == 0) { kk = idx % BK; jj = idx / BK; }
-      else { jj = idx % BN; kk = idx / BN; }
-      const int gj = j0 + jj, gkk = k0_ + kk;
-      const bool ok = gj < n && gkk < kd;
-      const double* src = T.tb == 0 ? T.b + (ok ? gkk + (size_t)gj * T.ldb : 0)
-                                    : T.b + (ok ? gj + (size_t)gkk * T.ldb : 0);
-      cp_async8_zfill(&Bs[buf][kk][jj], src, ok);
+      for (int e = 0; e < EB; e += 2) {
+        int jj, kk;
+        b_elem(e, true, 1, jj, kk);
+        const int gj = j0 + jj, gkk = k0_ + kk;
+        const int nv = gkk < kd ? min(max(n - gj, 0), 2) : 0;
+        cp_async16_zfill(&Bs[buf][kk][jj], T.b + (nv ? gj + (size_t)gkk * T.ldb : 0), 8 * nv);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < EB; ++e) {
+        int jj, kk;
+        b_elem(e, false, T.tb, jj, kk);
+        const int gj = j0 + jj, gkk = k0_ + kk;
+        const bool ok = gj < n && gkk < kd;
+        const double* src = T.tb == 0 ? T.b + (ok ? gkk + (size_t)gj * T.ldb : 0)
+                                      : T.b + (ok ? gj + (size_t)gkk * T.ldb : 0);
+        cp_async8_zfill(&Bs[buf][kk][jj], src, ok);
+      }
     }
   };
   // masks / alpha on the elements this thread staged (after they landed)
   auto fixup = [&](int buf, int ti_, int k0_) {
     const hq_gemm_term T = terms[P.term0 + ti_];
     if (T.mask_a != 0) {
+      const bool va = vec_a(T);
 #pragma unroll
       for (int e = 0; e < EA; ++e) {
-        const int idx = t + e * NTH;
         int ii, kk;
-        if (T.ta == 0) { ii = idx % BM; kk = idx / BM; }
-        else { kk = idx % BK; ii = idx / BK; }
+        a_elem(e, va, T.ta, ii, kk);
         const int gi = i0 + ii, gkk = k0_ + kk;
         double& v = As[buf][kk][ii];
         v = T.ta == 0 ? hq_mask(v, gi, gkk, T.mask_a) : hq_mask(v, gkk, gi, T.mask_a);
       }
     }
     if (T.mask_b != 0 || T.alpha != 1.0) {
+      const bool vb = vec_b(T);
 #pragma unroll
       for (int e = 0; e < EB; ++e) {
-        const int idx = t + e * NTH;
         int jj, kk;
-        if (T.tb == 0) { kk = idx % BK; jj = idx / BK; }
-        else { jj = idx % BN; kk = idx / BN; }
+        b_elem(e, vb, T.tb, jj, kk);
         const int gj = j0 + jj, gkk = k0_ + kk;
         double& v = Bs[buf][kk][jj];
         const double w = T.tb == 0 ? hq_mask(v, gkk, gj, T.mask_b) : hq_mask(v, gj, gkk, T.mask_b);
