@@ -199,7 +199,7 @@ typedef struct hq_rowblk_prob {
 /* ---- launchers ---------------------------------------------------------- */
 /* bumped whenever a descriptor layout or a launcher signature changes;
    the Python binding refuses a library with another version */
-#define HQ_ABI_VERSION 5
+#define HQ_ABI_VERSION 6
 int hq_abi_version(void);
 int hq_device_check(void);
 
@@ -241,8 +241,14 @@ int hq_concat(void* stream, const hq_concat_prob* probs, int nprob, const hq_pie
    blocks round-robin, panel factorization overlapped with the trailing
    updates of the previous panel); requires tpanel != NULL */
 int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank, int cluster);
-/* grid = nprob x ceil(max_cols / 32): column chunks of X run on separate CTAs */
-int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank, int max_cols);
+/* grid = nprob x ceil(max_cols / cw): column chunks of X run on separate
+   CTAs.  max_rows bounds m over the launch (0: unknown) and sizes the shared
+   memory: the chunk (cw = 32, 16 or 8 columns, the widest that fits beside a
+   16-reflector panel of max_rows rows) stays in shared memory while the
+   panels stream through it by bulk copies; problems taller than what fits
+   with cw = 8 (about 1090 rows) run from global memory */
+int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank, int max_cols,
+              int max_rows);
 /* cluster >= 2: one-sided block Jacobi on a cluster of `cluster` CTAs (2, 4
    or 8) per problem, X distributed over their shared memories (DSMEM);
    max_m bounds the row count (<= 512) and selects the lane-group width.

@@ -69,7 +69,7 @@ SIGNATURES = {
     "hq_gemm_skinny": [_vp, _vp, _i, _vp, _vp, _i, _i, _i, _i, _vp],
     "hq_concat": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_qr": [_vp, _vp, _i, _vp, _i],
-    "hq_applyq": [_vp, _vp, _i, _vp, _i],
+    "hq_applyq": [_vp, _vp, _i, _vp, _i, _i],
     "hq_svd": [_vp, _vp, _i, _vp, _vp, _i, _i, _i],
     "hq_svd_block": [_vp, _vp, _i, _vp, _vp, _i],
     "hq_qrcp": [_vp, _vp, _i, _vp, _vp, _i, _i, _i],
@@ -83,7 +83,7 @@ SIGNATURES = {
 }
 
 _LIB = None
-ABI_VERSION = 5   # HQ_ABI_VERSION in include/hodlrqr_b200.h
+ABI_VERSION = 6   # HQ_ABI_VERSION in include/hodlrqr_b200.h
 
 
 class LibraryError(RuntimeError):

@@ -120,6 +120,48 @@ HQ_DEV void cp_async16(void* smem, const void* gmem) {
 }
 HQ_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// ---- 1-D bulk copies on the TMA engine (cp.async.bulk: no tensor map, the
+// source is any 16-byte aligned run of a multiple of 16 bytes -- a column of
+// a column-major operand).  Loads complete on an mbarrier (transaction
+// bytes), stores in a bulk group.
+HQ_DEV void mbar_init(unsigned long long* bar, int count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+HQ_DEV void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes) : "memory");
+}
+HQ_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "HQ_MBAR_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@p bra HQ_MBAR_DONE;\n"
+      "bra HQ_MBAR_WAIT;\n"
+      "HQ_MBAR_DONE:\n"
+      "}\n" ::"r"(a), "r"(parity) : "memory");
+}
+HQ_DEV void bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const unsigned ba = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(sa),
+               "l"(gmem), "r"(bytes), "r"(ba)
+               : "memory");
+}
+HQ_DEV void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gmem), "r"(sa), "r"(bytes)
+               : "memory");
+}
+HQ_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+HQ_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+// generic-proxy writes to shared memory -> visible to the bulk-copy engine
+HQ_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 // d += A(8 x K) B(K x 8) over k in [kb, ke) on the FP64 tensor pipe with a
 // two-stage register pipeline: the operands of the next 32 k-steps are in
 // flight while the current 8 mma.sync run.  fetch(k0, av, bv) fills the

@@ -7,6 +7,7 @@
 // One CTA per problem; panels of NB columns are staged in shared memory when
 // they fit, otherwise reduced in place in (L2-resident) global memory.
 #include "hq_common.cuh"
+#include <cstdlib>
 #include <cooperative_groups.h>
 namespace cg = cooperative_groups;
 
@@ -319,6 +320,52 @@ __device__ __forceinline__ void stage_cols(double* dst, int ldd, const double* s
   }
   cp_async_wait_all();
   __syncthreads();
+}
+
+// stage_cols with the columns moved by the TMA engine: one cp.async.bulk per
+// column (the even part of the rows; an odd last row by a plain copy),
+// completion on the mbarrier `bar` whose phase parity the caller carries in
+// `parity`.  Falls back to stage_cols when a column start is not 16-byte
+// aligned.  Block-uniform; ends with a barrier.
+__device__ __forceinline__ void stage_cols_bulk(double* dst, int ldd, const double* src, int lds, int rows, int cols,
+                                                unsigned long long* bar, unsigned& parity) {
+  const int re = rows & ~1;
+  const bool ok = ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) && ((lds | ldd) & 1) == 0 && re > 0 && cols > 0;
+  if (!ok) { stage_cols(dst, ldd, src, lds, rows, cols); return; }
+  const int t = threadIdx.x;
+  if (t < 32) {
+    if (t == 0) mbar_expect_tx(bar, (unsigned)cols * (unsigned)re * 8u);
+    __syncwarp();
+    for (int c = t; c < cols; c += 32) bulk_g2s(dst + (size_t)c * ldd, src + (size_t)c * lds, (unsigned)re * 8u, bar);
+  } else if (rows & 1) {
+    for (int c = t - 32; c < cols; c += NT - 32) dst[re + (size_t)c * ldd] = src[re + (size_t)c * lds];
+  }
+  mbar_wait(bar, parity);
+  parity ^= 1u;
+  __syncthreads();
+}
+
+// shared -> global write-back of cols columns by bulk copies (same alignment
+// rule; plain stores otherwise).  The caller's last writes to src must be
+// separated from this call by a barrier only (the proxy fence is here).
+__device__ __forceinline__ void store_cols_bulk(double* dst, int ldd, const double* src, int lds, int rows, int cols) {
+  const int re = rows & ~1;
+  const bool ok = ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) && ((lds | ldd) & 1) == 0 && re > 0;
+  const int t = threadIdx.x;
+  if (!ok) {
+    for (int j = 0; j < cols; ++j)
+      for (int i = t; i < rows; i += NT) dst[i + (size_t)j * ldd] = src[i + (size_t)j * lds];
+    return;
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  if (t < 32) {
+    for (int c = t; c < cols; c += 32) bulk_s2g(dst + (size_t)c * ldd, src + (size_t)c * lds, (unsigned)re * 8u);
+    bulk_commit();
+    bulk_wait_all();
+  } else if (rows & 1) {
+    for (int c = t - 32; c < cols; c += NT - 32) dst[re + (size_t)c * ldd] = src[re + (size_t)c * lds];
+  }
 }
 
 // X (rows x ncols) := (I - Y T^op Y^T) X for panel reflectors Y (rows x pw,
@@ -839,63 +886,121 @@ __global__ void __launch_bounds__(NT, 1) qr_cluster_kernel(const hq_qr_prob* __r
   }
 }
 
-// grid (problem, column chunk of APQ_CW): the columns of X are independent,
-// so each CTA applies all reflectors to its own chunk.  For m <= APQ_STAGE
-// the chunk stays in shared memory for the whole sweep over the panels and
-// each panel's reflectors are staged with asynchronous copies.
-constexpr int APQ_CW = 32;
-constexpr int APQ_STAGE = 512;
+// grid (problem, column chunk of cwk): the columns of X are independent, so
+// each CTA applies all reflectors to its own chunk.  The launch sizes the
+// shared memory for its tallest problem (ldcap = pad_ld(max rows)): the chunk
+// of X (cwk = 32, 16 or 8 columns, the widest that fits beside one panel of
+// reflectors) stays in shared memory for the whole sweep over the panels, and
+// every panel's reflectors and T factor arrive by bulk copies (one
+// cp.async.bulk per column, completion on an mbarrier) -- into the other of
+// two buffers while the current panel is applied when both fit (nbuf = 2).
+// Problems taller than the launch's capacity (ldcap = 0: none staged) run
+// from global memory.
 struct ApqSmem {
-  double tp[NB * NB];
+  double tp[2][NB * NB];
   double wsp[WSP];
-  double xbuf[(APQ_STAGE + 16) * APQ_CW];
-  double ybuf[(APQ_STAGE + 16) * NB];
+  unsigned long long bar[4];   // [0], [1]: panel buffers; [2]: the chunk of X
 };
+static_assert(sizeof(ApqSmem) % 16 == 0, "staging buffers follow ApqSmem 16-byte aligned");
+// apply_panel_cols reads S.wsp only
+constexpr int APQ_SMEM_MAX = 232448;   // opt-in shared memory per CTA (227 KB)
 
 __global__ void __launch_bounds__(NT) applyq_kernel(const hq_applyq_prob* __restrict__ probs,
-                                                    int* __restrict__ rank) {
+                                                    int* __restrict__ rank, int cwk, int ldcap, int nbuf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ApqSmem& S = *reinterpret_cast<ApqSmem*>(smem_raw);
+  double* const xbuf = reinterpret_cast<double*>(smem_raw + sizeof(ApqSmem));
+  double* const ybuf0 = xbuf + (size_t)ldcap * cwk;
+  double* const ybuf1 = nbuf == 2 ? ybuf0 + (size_t)ldcap * NB : ybuf0;
   const hq_applyq_prob A = probs[blockIdx.x];
   const int m = hq_dim(rank, A.m, A.m_ri), k = hq_dim(rank, A.k, A.k_ri);
   const int call = hq_dim(rank, A.c, A.c_ri);
   const int r = m < k ? m : k;
   const int t = threadIdx.x;
-  const int cbeg = blockIdx.y * APQ_CW;
+  const int cbeg = blockIdx.y * cwk;
   if (m <= 0 || cbeg >= call) return;
-  const int c = min(APQ_CW, call - cbeg);
+  const int c = min(cwk, call - cbeg);
   double* Xg = A.x + (size_t)cbeg * A.ldx;
-  const bool staged = m <= APQ_STAGE;
-  double* X = staged ? S.xbuf : Xg;
-  const int ldx = staged ? pad_ld(m) : A.ldx;
+  const bool staged = ldcap > 0 && pad_ld(m) <= ldcap;
+  const int np = (r + NB - 1) / NB;
+  if (!staged) {
+    // ---- global-memory path
+    if (A.x0) {
+      const int r0 = hq_dim(rank, A.r0, A.r0_ri);
+      const double* X0 = A.x0 + (size_t)cbeg * A.ldx0;
+      for (int j = 0; j < c; ++j)
+        for (int i = t; i < m; i += NT) Xg[i + (size_t)j * A.ldx] = i < r0 ? X0[i + (size_t)j * A.ldx0] : 0.0;
+      __syncthreads();
+    }
+    for (int s = 0; s < np; ++s) {
+      const int p = A.trans ? s : np - 1 - s;
+      const int p0 = p * NB, pw = min(NB, r - p0), rows = m - p0;
+      if (t < NB * NB) S.tp[0][t] = A.tpanel[(size_t)p * NB * NB + t];
+      __syncthreads();
+      apply_panel_cols(A.w + p0 + (size_t)p0 * A.ldw, A.ldw, rows, pw, S.tp[0], Xg + p0, A.ldx, c, A.trans != 0, S);
+    }
+    return;
+  }
+  // ---- staged path
+  const int ldx = pad_ld(m);
+  const bool ybulk = ((((uintptr_t)A.w | (uintptr_t)A.tpanel) & 15) == 0) && (A.ldw & 1) == 0;
+  if (t == 0) { mbar_init(&S.bar[0], 1); mbar_init(&S.bar[1], 1); mbar_init(&S.bar[2], 1); }
+  __syncthreads();
+  unsigned par[2] = {0u, 0u};
+  // start the copy of panel step s (reflectors + T factor) into its buffer
+  auto issue = [&](int s) {
+    const int b = nbuf == 2 ? (s & 1) : 0;
+    const int p = A.trans ? s : np - 1 - s;
+    const int p0 = p * NB, pw = min(NB, r - p0), rows = m - p0;
+    const double* Y = A.w + p0 + (size_t)p0 * A.ldw;
+    const double* tpg = A.tpanel + (size_t)p * NB * NB;
+    double* yb = b ? ybuf1 : ybuf0;
+    const int ldy = pad_ld(rows);
+    if (ybulk) {
+      const int re = rows & ~1;
+      if (t < 32) {
+        if (t == 0) {
+          mbar_expect_tx(&S.bar[b], (unsigned)(pw * re + NB * NB) * 8u);
+          bulk_g2s(S.tp[b], tpg, NB * NB * 8u, &S.bar[b]);
+        }
+        __syncwarp();
+        if (re > 0 && t < pw) bulk_g2s(yb + (size_t)t * ldy, Y + (size_t)t * A.ldw, (unsigned)re * 8u, &S.bar[b]);
+      } else if (rows & 1) {
+        for (int j = t - 32; j < pw; j += NT - 32) yb[re + (size_t)j * ldy] = Y[re + (size_t)j * A.ldw];
+      }
+    } else {
+      if (t < NB * NB) S.tp[b][t] = tpg[t];
+      for (int j = 0; j < pw; ++j)
+        for (int i = t; i < rows; i += NT) cp_async8(yb + i + (size_t)j * ldy, Y + i + (size_t)j * A.ldw);
+    }
+  };
+  auto arrived = [&](int s) {
+    const int b = nbuf == 2 ? (s & 1) : 0;
+    if (ybulk) { mbar_wait(&S.bar[b], par[b]); par[b] ^= 1u; }
+    else cp_async_wait_all();
+    __syncthreads();
+  };
+  if (np > 0) issue(0);
   if (A.x0) {
     const int r0 = hq_dim(rank, A.r0, A.r0_ri);
     const double* X0 = A.x0 + (size_t)cbeg * A.ldx0;
     for (int j = 0; j < c; ++j)
-      for (int i = t; i < m; i += NT) X[i + (size_t)j * ldx] = i < r0 ? X0[i + (size_t)j * A.ldx0] : 0.0;
-    __syncthreads();
-  } else if (staged) {
-    stage_cols(S.xbuf, ldx, Xg, A.ldx, m, c);
+      for (int i = t; i < m; i += NT) xbuf[i + (size_t)j * ldx] = i < r0 ? X0[i + (size_t)j * A.ldx0] : 0.0;
+  } else {
+    unsigned px = 0;
+    stage_cols_bulk(xbuf, ldx, Xg, A.ldx, m, c, &S.bar[2], px);
   }
-  const int np = (r + NB - 1) / NB;
   for (int s = 0; s < np; ++s) {
+    if (nbuf == 2 && s + 1 < np) issue(s + 1);
+    arrived(s);   // its barrier also publishes the chunk of X before the first panel
+    const int b = nbuf == 2 ? (s & 1) : 0;
     const int p = A.trans ? s : np - 1 - s;
     const int p0 = p * NB, pw = min(NB, r - p0), rows = m - p0;
-    if (t < NB * NB) S.tp[t] = A.tpanel[(size_t)p * NB * NB + t];
-    const double* Y = A.w + p0 + (size_t)p0 * A.ldw;
-    int ldy = A.ldw;
-    if (staged) {
-      ldy = pad_ld(rows);
-      stage_cols(S.ybuf, ldy, Y, A.ldw, rows, pw);
-      Y = S.ybuf;
-    } else {
-      __syncthreads();
-    }
-    apply_panel_cols(Y, ldy, rows, pw, S.tp, X + p0, ldx, c, A.trans != 0, S);
+    apply_panel_cols(b ? ybuf1 : ybuf0, pad_ld(rows), rows, pw, S.tp[b], xbuf + p0, ldx, c, A.trans != 0, S);
+    if (nbuf == 1 && s + 1 < np) issue(s + 1);
   }
-  if (staged)
-    for (int j = 0; j < c; ++j)
-      for (int i = t; i < m; i += NT) Xg[i + (size_t)j * A.ldx] = X[i + (size_t)j * ldx];
+  if (np == 0) __syncthreads();
+  store_cols_bulk(Xg, A.ldx, xbuf, ldx, m, c);
 }
 
 // dst (rows x K) = [alpha_1 P_1 | alpha_2 P_2 | ...]; K -> rank[ktot_ri]
@@ -1092,17 +1197,29 @@ extern "C" int hq_qr(void* stream, const hq_qr_prob* probs, int nprob, int* rank
 }
 
 extern "C" int hq_applyq(void* stream, const hq_applyq_prob* probs, int nprob, int* rank,
-                         int max_cols) {
+                         int max_cols, int max_rows) {
   if (nprob <= 0) return 0;
-  const int nchunk = max_cols > 0 ? (max_cols + APQ_CW - 1) / APQ_CW : 1;
   static bool attr = false;
+  static int force_cw = 0, force_nbuf = 0;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(applyq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(ApqSmem));
+    cudaError_t e = cudaFuncSetAttribute(applyq_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, APQ_SMEM_MAX);
     if (e != cudaSuccess) return hq_err(e);
+    if (const char* v = getenv("HQ_APQ_CW")) force_cw = atoi(v);       // experiments only
+    if (const char* v = getenv("HQ_APQ_NBUF")) force_nbuf = atoi(v);
     attr = true;
   }
-  applyq_kernel<<<dim3(nprob, nchunk), NT, sizeof(ApqSmem), (cudaStream_t)stream>>>(probs, rank);
+  // chunk width / buffers from the tallest problem of the launch (unknown: 512 rows)
+  const long long avail = (APQ_SMEM_MAX - (long long)sizeof(ApqSmem)) / 8;
+  const int ld = pad_ld(max_rows > 0 ? max_rows : 512);
+  int cwk = 0;
+  for (int cw : {32, 16, 8})
+    if ((long long)ld * (cw + NB) <= avail && (force_cw == 0 || cw <= force_cw)) { cwk = cw; break; }
+  int ldcap = ld, nbuf = 1;
+  if (cwk == 0 || force_cw < 0) { cwk = 32; ldcap = 0; }
+  else if ((long long)ld * (cwk + 2 * NB) <= avail && force_nbuf != 1) nbuf = 2;
+  const size_t smem = sizeof(ApqSmem) + (size_t)ldcap * (cwk + nbuf * NB) * 8;
+  const int nchunk = max_cols > 0 ? (max_cols + cwk - 1) / cwk : 1;
+  applyq_kernel<<<dim3(nprob, nchunk), NT, smem, (cudaStream_t)stream>>>(probs, rank, cwk, ldcap, nbuf);
   return hq_err(cudaGetLastError());
 }
 

@@ -634,10 +634,10 @@ class Builder:
         else:
             self.op("qr", qrc, dict(role="core"))
         self.op("svd", svd, svd_cluster(svd))
-        self.op("applyq", apq, dict(max_cols=max(p[10].cap for p in apq)))
+        self.op("applyq", apq, dict(max_cols=max(p[10].cap for p in apq), max_rows=max(p[8].cap for p in apq)))
         if unstack:
             self.op("rowblk", unstack, dict(max_chunks=maxch))
-            self.op("applyq", apq2, dict(max_cols=max(p[10].cap for p in apq2)))
+            self.op("applyq", apq2, dict(max_cols=max(p[10].cap for p in apq2), max_rows=max(p[8].cap for p in apq2)))
         self.gemm(gm_m)
         self.gemm(gm_v)
 
@@ -1525,7 +1525,7 @@ class CompiledPlan:
                     rc = lib.hq_svd(stream_handle, dp + o1, cnt, rk, sc, ex.get("cluster", 1), ex.get("max_m", 0),
                                     ex.get("small", 0))
             elif kind == "applyq":
-                rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk, ex.get("max_cols", 0))
+                rc = lib.hq_applyq(stream_handle, dp + o1, cnt, rk, ex.get("max_cols", 0), ex.get("max_rows", 0))
             elif kind == "leaf_gather":
                 rc = lib.hq_leaf_gather(stream_handle, dp + o1, cnt, dp + o2, rk, ex["max_nl"])
             elif kind == "leaf_scatter":

@@ -220,10 +220,61 @@ def test_qr_and_applyq(dev, m, k, cl):
     ap[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), dX.data_ptr(), dX0.data_ptr(), m, m, r,
              m, -1, k, -1, c, -1, r, -1, 0)
     da = put(torch, ap)
-    assert lib.hq_applyq(None, da.data_ptr(), 1, rank.data_ptr(), c) == 0
+    assert lib.hq_applyq(None, da.data_ptr(), 1, rank.data_ptr(), c, m if cl != 2 else 0) == 0
     torch.cuda.synchronize()
     ref = Q[:, :r] @ X0
     assert np.abs(back(dX, m, c) - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("trans,max_rows", [(0, None), (1, None), (0, 0), (1, 1024)])
+@pytest.mark.parametrize("m,k,c,ldx,off", [(64, 48, 40, 64, 0), (65, 33, 7, 66, 0), (65, 33, 7, 65, 0),
+                                            (200, 150, 70, 202, 1), (200, 150, 70, 200, 2), (2, 2, 3, 2, 0),
+                                            (1, 1, 2, 2, 0), (511, 100, 33, 512, 0), (700, 40, 20, 700, 0)])
+def test_applyq_in_place(dev, m, k, c, ldx, off, trans, max_rows):
+    """X := Q X / Q^T X in place (x0 = NULL): the staged path moves the columns
+    of X and of every reflector panel with bulk copies when their starts are
+    16-byte aligned (even ld, even offset) and with element copies otherwise;
+    odd row counts, rows > 512 (X left in global memory)."""
+    # max_rows: the launch's row bound (None: exact; 0: unknown -> 512, taller
+    # problems run from global memory; 1024: 8-column chunks, one panel buffer)
+    max_rows = m if max_rows is None else max_rows
+    torch, lib = dev
+    rng = np.random.default_rng(m * 31 + k + c)
+    A = rng.standard_normal((m, k))
+    dW = colmajor(torch, A)
+    r = min(m, k)
+    tau = torch.zeros(max(r, 1), dtype=torch.float64, device="cuda")
+    tp = torch.zeros(((r + 15) // 16) * 256 + 2 * r * 16 + 256, dtype=torch.float64, device="cuda")
+    tf = torch.zeros(r * r + 32 * r, dtype=torch.float64, device="cuda")
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    q = np.zeros(1, _abi.QR_PROB)
+    q[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), tf.data_ptr(), m, r, m, -1, k, -1)
+    assert lib.hq_qr(None, put(torch, q).data_ptr(), 1, rank.data_ptr(), 1) == 0
+    torch.cuda.synchronize()
+    W = back(dW, m, k)
+    Y = np.tril(W[:, :r], -1)
+    Y[np.arange(r), np.arange(r)] = 1.0
+    T = np.triu(back(tf[:r * r], r, r))
+    Q = np.eye(m) - Y @ T @ Y.T
+    X = rng.standard_normal((m, c))
+    buf = np.full(off + ldx * c + 8, 7.5)
+    for j in range(c):
+        buf[off + j * ldx: off + j * ldx + m] = X[:, j]
+    dX = torch.tensor(buf, device="cuda")
+    ap = np.zeros(1, _abi.APPLYQ_PROB)
+    ap[0] = (dW.data_ptr(), tau.data_ptr(), tp.data_ptr(), dX.data_ptr() + 8 * off, 0, m, ldx, 0,
+             m, -1, k, -1, c, -1, 0, -1, trans)
+    assert lib.hq_applyq(None, put(torch, ap).data_ptr(), 1, rank.data_ptr(), c, max_rows) == 0
+    torch.cuda.synchronize()
+    out = dX.cpu().numpy()
+    ref = (Q.T if trans else Q) @ X
+    got = np.stack([out[off + j * ldx: off + j * ldx + m] for j in range(c)], axis=1)
+    assert np.abs(got - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
+    # nothing outside the m x c block was touched
+    out2 = out.copy()
+    for j in range(c):
+        out2[off + j * ldx: off + j * ldx + m] = 7.5
+    assert (out2 == 7.5).all()
 
 
 @pytest.mark.parametrize("xform,CL", [(0, 1), (1, 1), (1, 2), (1, 4), (1, 8), (1, 16), (0, 0), (1, 0)])
