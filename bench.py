@@ -499,7 +499,7 @@ def main():
         clear_engines()
     if not args.no_instrument and rank == 0:
         per, skipped = instrument(eng, torch)
-        acc = plan_accounting(eng.builder, rk, skipped)
+        acc = plan_accounting(eng.builder, rk, skipped, rk_in=eng.rk)
         tot = sum(v[0] for v in per.values())
         kinds = {k: {"ms": v[0], "launches": v[1], "share": v[0] / tot,
                      "gflop": acc.get(k, {}).get("flops", 0.0) / 1e9,

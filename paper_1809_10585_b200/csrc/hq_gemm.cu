@@ -423,11 +423,16 @@ __global__ void __launch_bounds__(NT) gemm_rows_kernel(const hq_gemm_prob* __res
 //               k, warp-shuffle reduction, shared-memory accumulation.
 // B (k x NC) is tiny and read through the cache.  K-split slices add into C
 // atomically (the caller zeroed C).
-constexpr int GV_ROWS = 64, GV_U = 8, GV_RQH = 4;
+constexpr int GV_U = 8, GV_RQH = 4;
+// output rows per CTA from the launch's tallest problem (plan.py gv_rows is
+// the same rule): a 256-row leaf as ONE band reads whole 2 KB columns -- 64-row
+// bands (512-byte pieces at a 2 KB stride, the four bands of a leaf on
+// different SMs at different times) reached 4.4 TB/s, 128-row bands 5.4
+__host__ __device__ constexpr int gv_rows(int max_rows) { return max_rows >= 256 ? 256 : (max_rows >= 128 ? 128 : 64); }
 // KIND 0: terms of both layouts; 1: only op(A) = A; 2: only op(A) = A^T
 // (the planner knows each launch's layouts; the lean variants keep fewer
 // registers live and run more warps per SM)
-template <int NC, int KIND>
+template <int NC, int KIND, int GV_ROWS>
 __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm_prob* __restrict__ probs,
                                                   const hq_gemm_term* __restrict__ terms,
                                                   const int* __restrict__ rank, int ksplit,
@@ -443,8 +448,9 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
   __shared__ double part[NT / GV_ROWS][GV_ROWS][NC];
   // A^T-layout sums per k-lane group (a row is shared by up to 8 warps:
   // separate slots, added in a fixed order -- no shared-memory atomics)
-  __shared__ double dotr[8][GV_ROWS][NC];
-  for (int e = t; e < 8 * GV_ROWS * NC; e += NT) (&dotr[0][0][0])[e] = 0.0;
+  constexpr int DQ = GV_ROWS >= 256 ? 2 : 8;   // k-lane groups per row (few-row blocks only)
+  __shared__ double dotr[DQ][GV_ROWS][NC];
+  for (int e = t; e < DQ * GV_ROWS * NC; e += NT) (&dotr[0][0][0])[e] = 0.0;
   __syncthreads();
   const int r = t % GV_ROWS, sl = t / GV_ROWS;
   constexpr int NSL = NT / GV_ROWS;
@@ -462,7 +468,7 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
   if (z >= ks) return;
   // warps per A^T row: spread few rows over all warps
   int wpr = 1;
-  while (wpr < 8 && nr * wpr * 2 <= 8) wpr *= 2;
+  while (wpr < DQ && nr * wpr * 2 <= 8) wpr *= 2;
   for (int ti = 0; ti < P.nterm; ++ti) {
     const hq_gemm_term T = terms[P.term0 + ti];
     const int kd = hq_dim(rank, T.k, T.k_ri);
@@ -539,7 +545,43 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
         for (int q = 0; q < GV_RQH; ++q) rv[q] = qc + q < nq;
         const double* apc = ap0 + (size_t)qc * rstep;
         if (plain) {
-          for (int k = kb + sub * 32 + lane; k < ke; k += st) {
+          // 16-byte loads along k, two 64-wide steps in flight (even leading
+          // dims, 16-byte aligned bases, even slice start); the k-lane groups
+          // of a row interleave whole steps; the rest of the slice goes by
+          // the element loop below
+          const bool vec = T.tb == 0 && ((T.lda | T.ldb) & 1) == 0 && (kb & 1) == 0 &&
+                           (((uintptr_t)T.a | (uintptr_t)T.b) & 15) == 0;
+          const int stv = 64 * wpr;
+          const int kvend = vec ? kb + ((ke - kb) / stv) * stv : kb;
+          if (vec) {
+            auto step = [&](int kr, double2 (&a2)[GV_RQH], double2 (&b2)[NC]) {
+#pragma unroll
+              for (int j = 0; j < NC; ++j) b2[j] = __ldg(reinterpret_cast<const double2*>(T.b + bj[j] + kr) + lane);
+#pragma unroll
+              for (int q = 0; q < GV_RQH; ++q)
+                a2[q] = __ldg(reinterpret_cast<const double2*>(apc + (rv[q] ? q * rstep : 0) + kr) + lane);
+            };
+            auto fmas = [&](const double2 (&a2)[GV_RQH], const double2 (&b2)[NC]) {
+#pragma unroll
+              for (int q = 0; q < GV_RQH; ++q)
+#pragma unroll
+                for (int j = 0; j < NC; ++j) d[q][j] = fma(a2[q].y, b2[j].y, fma(a2[q].x, b2[j].x, d[q][j]));
+            };
+            int kr = kb + sub * 64;
+            for (; kr + stv < kvend; kr += 2 * stv) {
+              double2 a0[GV_RQH], b0[NC], a1[GV_RQH], b1[NC];
+              step(kr, a0, b0);
+              step(kr + stv, a1, b1);
+              fmas(a0, b0);
+              fmas(a1, b1);
+            }
+            if (kr < kvend) {
+              double2 a0[GV_RQH], b0[NC];
+              step(kr, a0, b0);
+              fmas(a0, b0);
+            }
+          }
+          for (int k = kvend + sub * 32 + lane; k < ke; k += st) {
             double b[NC], a[GV_RQH];
 #pragma unroll
             for (int j = 0; j < NC; ++j) b[j] = __ldg(T.b + (size_t)k * sbk + bj[j]);
@@ -583,7 +625,7 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
     if (j >= n) continue;
     double v = 0.0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v += dotr[q][rr][j];
+    for (int q = 0; q < DQ; ++q) v += dotr[q][rr][j];
 #pragma unroll
     for (int q = 0; q < NSL; ++q) v += part[q][rr][j];
     if (ks > 1) {
@@ -710,6 +752,28 @@ __global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __res
         const double2* bcol[NC];
 #pragma unroll
         for (int j = 0; j < NC; ++j) bcol[j] = reinterpret_cast<const double2*>(T.b + (size_t)(j < n ? j : 0) * T.ldb);
+        // rank-16 inputs leave a warp 2 rows: four steps in flight instead
+        // (the same 8 independent 16-byte loads of A per lane)
+        if (nq <= 2) {
+          for (; k + 256 <= ke; k += 256) {
+            double2 b[4][NC], av[4][2];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const int kk = (k + 64 * h) / 2 + lane;
+#pragma unroll
+              for (int j = 0; j < NC; ++j) b[h][j] = __ldg(bcol[j] + kk);
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+                av[h][q] = __ldg(reinterpret_cast<const double2*>(ap0 + (q < nq ? q * rstep : 0)) + kk);
+            }
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+#pragma unroll
+              for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int j = 0; j < NC; ++j) d[q][j] = fma(av[h][q].y, b[h][j].y, fma(av[h][q].x, b[h][j].x, d[q][j]));
+          }
+        }
         for (; k + 128 <= ke; k += 128) {
           double2 b[2][NC], av[2][RQ];
 #pragma unroll
@@ -785,15 +849,23 @@ extern "C" int hq_gemm_skinny(void* stream, const hq_gemm_prob* probs, int nprob
     return hq_err(cudaGetLastError());
   }
   if (mode >= 2 && mode <= 4) {
-    dim3 grid((max_rows + GV_ROWS - 1) / GV_ROWS, nprob, ksplit);
+    const int R = gv_rows(max_rows);
+    dim3 grid((max_rows + R - 1) / R, nprob, ksplit);
     const int kind = mode - 2;
+#define HQ_GEMV_LAUNCH(NC_, KIND_)                                                                          \
+  do {                                                                                                      \
+    if (R == 256) gemv_kernel<NC_, KIND_, 256><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);      \
+    else if (R == 128) gemv_kernel<NC_, KIND_, 128><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip); \
+    else gemv_kernel<NC_, KIND_, 64><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);                \
+  } while (0)
     if (ncmax <= 2) {
-      if (kind == 1) gemv_kernel<2, 1><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
-      else if (kind == 2) gemv_kernel<2, 2><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
-      else gemv_kernel<2, 0><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+      if (kind == 1) HQ_GEMV_LAUNCH(2, 1);
+      else if (kind == 2) HQ_GEMV_LAUNCH(2, 2);
+      else HQ_GEMV_LAUNCH(2, 0);
     } else {
-      gemv_kernel<4, 0><<<grid, NT, 0, st>>>(probs, terms, rank, ksplit, skip);
+      HQ_GEMV_LAUNCH(4, 0);
     }
+#undef HQ_GEMV_LAUNCH
     return hq_err(cudaGetLastError());
   }
   if (mode == 1) {

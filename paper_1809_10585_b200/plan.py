@@ -46,7 +46,10 @@ SVD_MAX_N = 1024
 R_PERSIST, R_PHASE, R_APPLY, R_TRUNC, R_SMALL, R_IN, R_OUT, R_SHARED, R_WS = range(9)
 LANE_STRIDE = 10   # scratch region of lane l: base + LANE_STRIDE * l (l = 0 main chain)
 GEMM_BK = 16       # k-tile of gemm_kernel (hq_gemm.cu BK)
-GV_ROWS = 64       # output rows per CTA of gemv_kernel (hq_gemm.cu GV_ROWS)
+def gv_rows(max_rows):
+    """Output rows per CTA of gemv_kernel for a launch whose tallest problem
+    has max_rows rows (hq_gemm.cu gv_rows: the same rule)."""
+    return 256 if max_rows >= 256 else (128 if max_rows >= 128 else 64)
 SPLIT_TARGET = 2 * 2 * 148   # CTAs a K-split launch aims for (148 SMs)
 
 
@@ -388,7 +391,7 @@ class Builder:
             # split K only as far as the launch needs CTAs: about SPLIT_TARGET
             # of them (two waves of two per SM); a batch that already fills
             # the GPU keeps whole K (no partial-sum traffic or workspace)
-            blocks = math.ceil(mmax / GV_ROWS) if skinny else tiles
+            blocks = math.ceil(mmax / gv_rows(mmax)) if skinny else tiles
             ksplit = max(1, min(ksplit, math.ceil(SPLIT_TARGET / (len(probs) * blocks))))
         ex = dict(tiles=tiles, ksplit=ksplit, skip=skip, skinny=skinny, ncmax=ncmax,
                   mode=mode, max_rows=mmax, tile=tile)
@@ -401,7 +404,7 @@ class Builder:
                 if skinny:
                     ktot = sum(t[8].cap for t in p[5])
                     ks = min(ksplit, max(1, ktot // 512))
-                    blocks, per = math.ceil(p[2].cap / GV_ROWS), GV_ROWS * (2 if ncmax <= 2 else 4)
+                    blocks, per = math.ceil(p[2].cap / gv_rows(mmax)), gv_rows(mmax) * (2 if ncmax <= 2 else 4)
                 else:
                     nkt = sum(math.ceil(t[8].cap / GEMM_BK) for t in p[5])
                     ks = min(ksplit, max(1, nkt // 8))
@@ -1617,10 +1620,14 @@ def kind_key(kind, extra):
     return kind
 
 
-def plan_accounting(builder, rk, skipped=None):
+def plan_accounting(builder, rk, skipped=None, rk_in=None):
     """Per-kernel-class launches / flops / bytes of a finished run.
     skipped: indices of the ops that were no-ops in that run (the power
-    iteration's gated launches after convergence); None: count no gated op."""
+    iteration's gated launches after convergence); None: count no gated op.
+    rk_in: the rank table as uploaded (the INPUT's ranks): the gated ops --
+    the power iteration on the input matrix -- ran before the factorization
+    overwrote those slots with the factors' ranks, so their dimensions are
+    taken from it (the final table would overcount their bytes severalfold)."""
     acc = {}
     for i, (kind, probs, extra) in enumerate(builder.ops):
         a = acc.setdefault(kind_key(kind, extra), {"launches": 0, "flops": 0.0, "bytes": 0.0})
@@ -1628,9 +1635,10 @@ def plan_accounting(builder, rk, skipped=None):
         gated = extra.get("skip") is not None
         if probs is None or (gated and (skipped is None or i in skipped)):
             continue
-        a["flops"] += op_flops(kind, probs, rk)
-        a["bytes"] += op_bytes(kind, probs, rk) if kind != "gemm" or not extra.get("skinny") \
-            else gemv_bytes(probs, rk)
+        r = rk_in if gated and rk_in is not None else rk
+        a["flops"] += op_flops(kind, probs, r)
+        a["bytes"] += op_bytes(kind, probs, r) if kind != "gemm" or not extra.get("skinny") \
+            else gemv_bytes(probs, r)
     return acc
 
 

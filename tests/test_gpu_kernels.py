@@ -150,7 +150,9 @@ def test_gemm_skinny(dev, m, n, k, ta, tb, ks, masks, mode):
         ws, cnt = split_buffers(torch, ks, m * nc, 1)
     else:
         ks_cap = min(ks, max(1, (k + 5) // 512))
-        ws, cnt = split_buffers(torch, -(-m // 64) * ks_cap, 64 * nc, -(-m // 64))
+        from paper_1809_10585_b200.plan import gv_rows
+        R = gv_rows(m)   # output rows per CTA (launch max_rows = m)
+        ws, cnt = split_buffers(torch, -(-m // R) * ks_cap, R * nc, -(-m // R))
     probs = np.zeros(1, _abi.GEMM_PROB)
     beta = 0.5
     probs[0] = (dC.data_ptr(), m, m, -1, n, -1, 0, 2, 0, beta, ws.data_ptr(), cnt.data_ptr())

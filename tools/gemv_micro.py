@@ -29,7 +29,7 @@ for ta in (0, 1):
         terms[7 * p] = (L[p].data_ptr(), X[p].data_ptr(), 256, 256, ta, 0, 256, -1, 0, 0, 1.0)
         for q in range(6):
             terms[7 * p + 1 + q] = (U[p, q].data_ptr(), T[p, q].data_ptr(), 256, 16, 0, 0, 16, -1, 0, 0, 1.0)
-        probs[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, 7 * p, 7, 0, 0.0)
+        probs[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, 7 * p, 7, 0, 0.0, 0, 0)
     dt, dp = put(terms), put(probs)
     nbytes = (L.numel() + U.numel()) * 8
     for mode in ((0, 1, 2, 3) if ta == 0 else (0, 1, 2, 4)):
@@ -45,10 +45,10 @@ t1 = np.zeros(P, _abi.GEMM_TERM); p1 = np.zeros(P, _abi.GEMM_PROB)
 t2 = np.zeros(P * 6, _abi.GEMM_TERM); p2 = np.zeros(P, _abi.GEMM_PROB)
 for p in range(P):
     t1[p] = (L[p].data_ptr(), X[p].data_ptr(), 256, 256, 1, 0, 256, -1, 0, 0, 1.0)
-    p1[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, p, 1, 0, 0.0)
+    p1[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, p, 1, 0, 0.0, 0, 0)
     for q in range(6):
         t2[6 * p + q] = (U[p, q].data_ptr(), T[p, q].data_ptr(), 256, 16, 0, 0, 16, -1, 0, 0, 1.0)
-    p2[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, 6 * p, 6, 0, 1.0)
+    p2[p] = (C[p].data_ptr(), 256, 256, -1, 2, -1, 6 * p, 6, 0, 1.0, 0, 0)
 d1, q1, d2, q2 = put(t1), put(p1), put(t2), put(p2)
 us1 = timeit(lambda: lib.hq_gemm_skinny(None, q1.data_ptr(), P, d1.data_ptr(), rank.data_ptr(), 1, 2, 4, 256, None))
 us2 = timeit(lambda: lib.hq_gemm_skinny(None, q2.data_ptr(), P, d2.data_ptr(), rank.data_ptr(), 1, 2, 3, 256, None))
@@ -62,7 +62,7 @@ for K, cnt in ((8192, 2), (4096, 4), (1024, 16), (256, 64)):
     terms = np.zeros(Pp, _abi.GEMM_TERM); probs = np.zeros(Pp, _abi.GEMM_PROB)
     for p in range(Pp):
         terms[p] = (V[p].data_ptr(), X[p].data_ptr(), K, K, 1, 0, K, -1, 0, 0, 1.0)
-        probs[p] = (C[p].data_ptr(), 16, 16, -1, 2, -1, p, 1, 0, 0.0)
+        probs[p] = (C[p].data_ptr(), 16, 16, -1, 2, -1, p, 1, 0, 0.0, 0, 0)
     dt, dp = put(terms), put(probs)
     for mode, ks, mr in ((0, min(32, K // 256), 16), (2, min(32, K // 256), 16), (2, min(32, K // 256), 512)):
         us = timeit(lambda: (C.zero_(), lib.hq_gemm_skinny(None, dp.data_ptr(), Pp, dt.data_ptr(), rank.data_ptr(), ks, 2, mode, mr, None)))

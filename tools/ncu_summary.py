@@ -3,9 +3,19 @@ per-launch DRAM traffic, and the stall mix of the SASS source page."""
 import csv, subprocess, sys
 
 
+SEL = ()   # import filter: one result of a multi-kernel report
+
+
 def page(rep, name, extra=()):
-    out = subprocess.run(["ncu", "-i", rep, "--page", name, "--csv", *extra], capture_output=True, text=True).stdout
+    out = subprocess.run(["ncu", "-i", rep, "--page", name, "--csv", *SEL, *extra], capture_output=True, text=True).stdout
     return list(csv.reader(out.splitlines()))
+
+
+def count(rep):
+    rows = page(rep, "details")
+    if not rows or "ID" not in rows[0]:
+        return 0
+    return len({r[rows[0].index("ID")] for r in rows[1:] if r})
 
 
 def summary(rep):
@@ -49,5 +59,8 @@ def summary(rep):
 
 if __name__ == "__main__":
     for rep in sys.argv[1:]:
-        print(summary(rep))
-        print()
+        n = count(rep)
+        for i in range(max(n, 1)):
+            SEL = ("--launch-skip", str(i), "--launch-count", "1") if n > 1 else ()
+            print(summary(rep))
+            print()
