@@ -36,7 +36,7 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // (bank-conflict-free fragment fetches); masks and alpha are applied by the
 // thread that copied the element, before the barrier that publishes the tile.
 template <int BM, int BN, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* __restrict__ probs,
+__global__ void __launch_bounds__(WM * WN * 32, BM == 64 ? 3 : 4) gemm_kernel(const hq_gemm_prob* __restrict__ probs,
                                                             const hq_gemm_term* __restrict__ terms,
                                                             const int* __restrict__ rank, int ksplit,
                                                             const int* __restrict__ skip) {
@@ -67,9 +67,19 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
     if ((int)blockIdx.z >= ks) return;
   }
 
+  // staged tile of op(A): layout 0 = [k][i] (ld LDA), layout 1 = [i][k] (ld
+  // LDT) for operands whose k runs contiguously in memory (A with ta = 1, B
+  // with tb = 0), so that those too are copied 16 bytes at a time.  LDT = 20:
+  // the m8n8k4 fragment fetch (8 rows x 4 k) touches 8-byte banks 4 gq + tq
+  // (mod 16): two wavefronts per warp, the minimum for 256 bytes
   extern __shared__ __align__(16) double gsm[];
-  double (*As)[BK][LDA] = reinterpret_cast<double (*)[BK][LDA]>(gsm);
-  double (*Bs)[BK][LDB] = reinterpret_cast<double (*)[BK][LDB]>(gsm + STAGES * BK * LDA);
+  constexpr int LDT = BK + 4;
+  constexpr int ASZ = BK * LDA > BM * LDT ? BK * LDA : BM * LDT;
+  constexpr int BSZ = BK * LDB > BN * LDT ? BK * LDB : BN * LDT;
+  double* const Asf = gsm;
+  double* const Bsf = gsm + STAGES * ASZ;
+  auto aidx = [&](int buf, bool tr, int kk, int ii) { return buf * ASZ + (tr ? ii * LDT + kk : kk * LDA + ii); };
+  auto bidx = [&](int buf, bool tr, int kk, int jj) { return buf * BSZ + (tr ? jj * LDT + kk : kk * LDB + jj); };
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
   const int gq = lane >> 2, tq = lane & 3;
   const int wm = wid % WM, wn = wid / WM;
@@ -99,69 +109,96 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
     advance(ti, k0, gk);
   }
   // element e of this thread's share of a staged k-tile -> (row/col, k).
-  // Operands whose rows are contiguous in memory (A with ta = 0, B with
-  // tb = 1) and 16-byte aligned are copied in pairs (elements 2p, 2p + 1 by
-  // the same thread: one 16-byte cp.async), the others one by one.
-  auto a_elem = [&](int e, bool vec, int ta, int& ii, int& kk) {
-    if (vec) { const int p = t + (e >> 1) * NTH; ii = 2 * (p % (BM / 2)) + (e & 1); kk = p / (BM / 2); }
-    else if (ta == 0) { const int idx = t + e * NTH; ii = idx % BM; kk = idx / BM; }
+  // Copy modes: 0 / 1 element by element (ta or tb = 0 / 1), 2 / 3 in pairs by
+  // one 16-byte cp.async when the operand is 16-byte aligned with an even
+  // leading dimension: 2 = pairs along the row index (A with ta = 0, B with
+  // tb = 1; layout [k][row]), 3 = pairs along k (A with ta = 1, B with
+  // tb = 0; layout [row][k]).
+  auto a_elem = [&](int e, int mode, int& ii, int& kk) {
+    if (mode == 2) { const int p = t + (e >> 1) * NTH; ii = 2 * (p % (BM / 2)) + (e & 1); kk = p / (BM / 2); }
+    else if (mode == 3) { const int p = t + (e >> 1) * NTH; kk = 2 * (p % (BK / 2)) + (e & 1); ii = p / (BK / 2); }
+    else if (mode == 0) { const int idx = t + e * NTH; ii = idx % BM; kk = idx / BM; }
     else { const int idx = t + e * NTH; kk = idx % BK; ii = idx / BK; }
   };
-  auto b_elem = [&](int e, bool vec, int tb, int& jj, int& kk) {
-    if (vec) { const int p = t + (e >> 1) * NTH; jj = 2 * (p % (BN / 2)) + (e & 1); kk = p / (BN / 2); }
-    else if (tb == 0) { const int idx = t + e * NTH; kk = idx % BK; jj = idx / BK; }
+  auto b_elem = [&](int e, int mode, int& jj, int& kk) {
+    if (mode == 2) { const int p = t + (e >> 1) * NTH; jj = 2 * (p % (BN / 2)) + (e & 1); kk = p / (BN / 2); }
+    else if (mode == 3) { const int p = t + (e >> 1) * NTH; kk = 2 * (p % (BK / 2)) + (e & 1); jj = p / (BK / 2); }
+    else if (mode == 0) { const int idx = t + e * NTH; kk = idx % BK; jj = idx / BK; }
     else { const int idx = t + e * NTH; jj = idx % BN; kk = idx / BN; }
   };
-  auto vec_a = [&](const hq_gemm_term& T) {
-    return T.ta == 0 && (((uintptr_t)T.a & 15) == 0) && (T.lda & 1) == 0;
+  auto mode_a = [&](const hq_gemm_term& T) {
+    const bool al = (((uintptr_t)T.a & 15) == 0) && (T.lda & 1) == 0;
+    return T.ta == 0 ? (al ? 2 : 0) : (al ? 3 : 1);
   };
-  auto vec_b = [&](const hq_gemm_term& T) {
-    return T.tb != 0 && (((uintptr_t)T.b & 15) == 0) && (T.ldb & 1) == 0;
+  auto mode_b = [&](const hq_gemm_term& T) {
+    const bool al = (((uintptr_t)T.b & 15) == 0) && (T.ldb & 1) == 0;
+    return T.tb != 0 ? (al ? 2 : 1) : (al ? 3 : 0);
   };
+  bool la[STAGES], lb[STAGES];   // layout of the tile in each ring buffer
   auto stage = [&](int buf, int ti_, int k0_) {
     const hq_gemm_term T = terms[P.term0 + ti_];
     const int kd = hq_dim(rank, T.k, T.k_ri);
-    const bool va = vec_a(T), vb = vec_b(T);
-    if (va) {
+    const int ma = mode_a(T), mb = mode_b(T);
+    la[buf] = ma == 3;
+    lb[buf] = mb == 3;
+    if (ma == 2) {
 #pragma unroll
       for (int e = 0; e < EA; e += 2) {
         int ii, kk;
-        a_elem(e, true, 0, ii, kk);
+        a_elem(e, 2, ii, kk);
         const int gi = i0 + ii, gkk = k0_ + kk;
         const int nv = gkk < kd ? min(max(m - gi, 0), 2) : 0;
-        cp_async16_zfill(&As[buf][kk][ii], T.a + (nv ? gi + (size_t)gkk * T.lda : 0), 8 * nv);
+        cp_async16_zfill(Asf + aidx(buf, false, kk, ii), T.a + (nv ? gi + (size_t)gkk * T.lda : 0), 8 * nv);
+      }
+    } else if (ma == 3) {
+#pragma unroll
+      for (int e = 0; e < EA; e += 2) {
+        int ii, kk;
+        a_elem(e, 3, ii, kk);
+        const int gi = i0 + ii, gkk = k0_ + kk;
+        const int nv = gi < m ? min(max(kd - gkk, 0), 2) : 0;
+        cp_async16_zfill(Asf + aidx(buf, true, kk, ii), T.a + (nv ? gkk + (size_t)gi * T.lda : 0), 8 * nv);
       }
     } else {
 #pragma unroll
       for (int e = 0; e < EA; ++e) {
         int ii, kk;
-        a_elem(e, false, T.ta, ii, kk);
+        a_elem(e, ma, ii, kk);
         const int gi = i0 + ii, gkk = k0_ + kk;
         const bool ok = gi < m && gkk < kd;
         const double* src = T.ta == 0 ? T.a + (ok ? gi + (size_t)gkk * T.lda : 0)
                                       : T.a + (ok ? gkk + (size_t)gi * T.lda : 0);
-        cp_async8_zfill(&As[buf][kk][ii], src, ok);
+        cp_async8_zfill(Asf + aidx(buf, false, kk, ii), src, ok);
       }
     }
-    if (vb) {
+    if (mb == 2) {
 #pragma unroll
       for (int e = 0; e < EB; e += 2) {
         int jj, kk;
-        b_elem(e, true, 1, jj, kk);
+        b_elem(e, 2, jj, kk);
         const int gj = j0 + jj, gkk = k0_ + kk;
         const int nv = gkk < kd ? min(max(n - gj, 0), 2) : 0;
-        cp_async16_zfill(&Bs[buf][kk][jj], T.b + (nv ? gj + (size_t)gkk * T.ldb : 0), 8 * nv);
+        cp_async16_zfill(Bsf + bidx(buf, false, kk, jj), T.b + (nv ? gj + (size_t)gkk * T.ldb : 0), 8 * nv);
+      }
+    } else if (mb == 3) {
+#pragma unroll
+      for (int e = 0; e < EB; e += 2) {
+        int jj, kk;
+        b_elem(e, 3, jj, kk);
+        const int gj = j0 + jj, gkk = k0_ + kk;
+        const int nv = gj < n ? min(max(kd - gkk, 0), 2) : 0;
+        cp_async16_zfill(Bsf + bidx(buf, true, kk, jj), T.b + (nv ? gkk + (size_t)gj * T.ldb : 0), 8 * nv);
       }
     } else {
 #pragma unroll
       for (int e = 0; e < EB; ++e) {
         int jj, kk;
-        b_elem(e, false, T.tb, jj, kk);
+        b_elem(e, mb, jj, kk);
         const int gj = j0 + jj, gkk = k0_ + kk;
         const bool ok = gj < n && gkk < kd;
         const double* src = T.tb == 0 ? T.b + (ok ? gkk + (size_t)gj * T.ldb : 0)
                                       : T.b + (ok ? gj + (size_t)gkk * T.ldb : 0);
-        cp_async8_zfill(&Bs[buf][kk][jj], src, ok);
+        cp_async8_zfill(Bsf + bidx(buf, false, kk, jj), src, ok);
       }
     }
   };
@@ -169,24 +206,24 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
   auto fixup = [&](int buf, int ti_, int k0_) {
     const hq_gemm_term T = terms[P.term0 + ti_];
     if (T.mask_a != 0) {
-      const bool va = vec_a(T);
+      const int ma = mode_a(T);
 #pragma unroll
       for (int e = 0; e < EA; ++e) {
         int ii, kk;
-        a_elem(e, va, T.ta, ii, kk);
+        a_elem(e, ma, ii, kk);
         const int gi = i0 + ii, gkk = k0_ + kk;
-        double& v = As[buf][kk][ii];
+        double& v = Asf[aidx(buf, ma == 3, kk, ii)];
         v = T.ta == 0 ? hq_mask(v, gi, gkk, T.mask_a) : hq_mask(v, gkk, gi, T.mask_a);
       }
     }
     if (T.mask_b != 0 || T.alpha != 1.0) {
-      const bool vb = vec_b(T);
+      const int mb = mode_b(T);
 #pragma unroll
       for (int e = 0; e < EB; ++e) {
         int jj, kk;
-        b_elem(e, vb, T.tb, jj, kk);
+        b_elem(e, mb, jj, kk);
         const int gj = j0 + jj, gkk = k0_ + kk;
-        double& v = Bs[buf][kk][jj];
+        double& v = Bsf[bidx(buf, mb == 3, kk, jj)];
         const double w = T.tb == 0 ? hq_mask(v, gkk, gj, T.mask_b) : hq_mask(v, gj, gkk, T.mask_b);
         v = w * T.alpha;
       }
@@ -212,13 +249,16 @@ __global__ void __launch_bounds__(WM * WN * 32) gemm_kernel(const hq_gemm_prob* 
     cp_async_wait<STAGES - 1>();
     fixup(buf, sti[buf], sk0[buf]);
     __syncthreads();
+    const bool tra = la[buf], trb = lb[buf];
+    const double* Ab = Asf + buf * ASZ;
+    const double* Bb = Bsf + buf * BSZ;
 #pragma unroll
     for (int kq = 0; kq < BK; kq += 4) {
       double av[TM], bv[TN];
 #pragma unroll
-      for (int a = 0; a < TM; ++a) av[a] = As[buf][kq + tq][(wm * TM + a) * 8 + gq];
+      for (int a = 0; a < TM; ++a) av[a] = Ab[tra ? ((wm * TM + a) * 8 + gq) * LDT + kq + tq : (kq + tq) * LDA + (wm * TM + a) * 8 + gq];
 #pragma unroll
-      for (int b = 0; b < TN; ++b) bv[b] = Bs[buf][kq + tq][(wn * TN + b) * 8 + gq];
+      for (int b = 0; b < TN; ++b) bv[b] = Bb[trb ? ((wn * TN + b) * 8 + gq) * LDT + kq + tq : (kq + tq) * LDB + (wn * TN + b) * 8 + gq];
 #pragma unroll
       for (int a = 0; a < TM; ++a)
 #pragma unroll
@@ -888,7 +928,7 @@ extern "C" int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob,
   dim3 grid(tiles, nprob, ksplit);
   cudaStream_t st = (cudaStream_t)stream;
   if (tile == 32) {
-    constexpr int S = 4, smem = S * BK * (36 + 36) * 8;
+    constexpr int S = 4, smem = S * 2 * (32 * (BK + 4) > BK * 36 ? 32 * (BK + 4) : BK * 36) * 8;
     static bool attr32 = false;
     if (!attr32) {
       cudaError_t e = cudaFuncSetAttribute(gemm_kernel<32, 32, 2, 2, S>,
@@ -898,7 +938,7 @@ extern "C" int hq_gemm_tiled(void* stream, const hq_gemm_prob* probs, int nprob,
     }
     gemm_kernel<32, 32, 2, 2, S><<<grid, 128, smem, st>>>(probs, terms, rank, ksplit, skip);
   } else {
-    constexpr int S = 3, smem = S * BK * (68 + 68) * 8;
+    constexpr int S = 3, smem = S * 2 * (64 * (BK + 4) > BK * 68 ? 64 * (BK + 4) : BK * 68) * 8;
     static bool attr = false;
     if (!attr) {
       cudaError_t e = cudaFuncSetAttribute(gemm_kernel<64, 64, 2, 4, S>,

@@ -4,6 +4,7 @@ import csv, subprocess, sys
 
 
 SEL = ()   # import filter: one result of a multi-kernel report
+SEL_INDEX = 0
 
 
 def page(rep, name, extra=()):
@@ -42,16 +43,25 @@ def summary(rep):
         if k in rh:
             out.append(f"  {k:70s} {row[rh.index(k)]} {raw[1][rh.index(k)]}")
     src = page(rep, "source", ("--print-source", "sass"))
-    for hi, r in enumerate(src):
-        if "Source" in r and len(r) > 5:
-            break
+    # a multi-kernel report prints one section per kernel, each with its own
+    # header row: take the section of the selected result
+    heads = [i for i, r in enumerate(src) if "Source" in r and len(r) > 5]
+    if not heads:
+        return "\n".join(out)
+    which = min(SEL_INDEX, len(heads) - 1) if len(heads) > 1 else 0
+    hi = heads[which]
     sh = src[hi]
-    data = src[hi + 1:]
+    data = [r for r in src[hi + 1:(heads[which + 1] if which + 1 < len(heads) else len(src))] if len(r) == len(sh)]
     if "Warp Stall Sampling (All Samples)" in sh:
         si2 = sh.index("Warp Stall Sampling (All Samples)")
         cols = [c for c in sh if c.startswith("stall_") and "Not Issued" not in c]
-        tot = sum(float(r[si2] or 0) for r in data) or 1.0
-        agg = {c: sum(float(r[sh.index(c)] or 0) for r in data) for c in cols}
+        def num(x):
+            try:
+                return float(x or 0)
+            except ValueError:
+                return 0.0
+        tot = sum(num(r[si2]) for r in data) or 1.0
+        agg = {c: sum(num(r[sh.index(c)]) for r in data) for c in cols}
         out.append("  stall mix (% of samples): " + ", ".join(
             f"{k[6:]} {100 * v / tot:.1f}" for k, v in sorted(agg.items(), key=lambda x: -x[1])[:8]))
     return "\n".join(out)
@@ -62,5 +72,9 @@ if __name__ == "__main__":
         n = count(rep)
         for i in range(max(n, 1)):
             SEL = ("--launch-skip", str(i), "--launch-count", "1") if n > 1 else ()
-            print(summary(rep))
+            SEL_INDEX = i
+            try:
+                print(summary(rep))
+            except Exception as e:   # noqa: BLE001
+                print("summary failed for result", i, repr(e))
             print()
