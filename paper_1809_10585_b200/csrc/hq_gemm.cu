@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_kernel(const hq_gemm
 // slices of a split problem write their own workspace slots and the last to
 // arrive sums them in slice order (deterministic).
 template <int NC>
-__global__ void __launch_bounds__(NT) gemv_flat_kernel(const hq_gemm_prob* __restrict__ probs,
+__global__ void __launch_bounds__(NT, NC == 2 ? 3 : 2) gemv_flat_kernel(const hq_gemm_prob* __restrict__ probs,
                                                        const hq_gemm_term* __restrict__ terms,
                                                        const int* __restrict__ rank, int nprob, int nitems,
                                                        const int* __restrict__ skip) {

@@ -1011,11 +1011,29 @@ __global__ void concat_kernel(const hq_concat_prob* __restrict__ probs,
   for (int q = 0; q < C.npiece; ++q) {
     const hq_piece Pc = pieces[C.piece0 + q];
     const int nc = hq_dim(rank, Pc.cols, Pc.cols_ri);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C.rows; i += gridDim.x * blockDim.x) {
-      for (int j = 0; j < nc; ++j) {
-        const double v = Pc.alpha * Pc.p[i + (size_t)j * Pc.ld];
-        C.dst[i + (size_t)(col + j) * C.ldd] = v;
-        if (C.dst2) C.dst2[i + (size_t)(col + j) * C.ldd2] = v;
+    // two rows per thread by 16-byte accesses when every column start is
+    // 16-byte aligned on all sides; four columns in flight either way
+    const bool vec = (C.rows & 1) == 0 && ((Pc.ld | C.ldd | (C.dst2 ? C.ldd2 : 0)) & 1) == 0 &&
+                     ((((uintptr_t)Pc.p | (uintptr_t)C.dst | (uintptr_t)C.dst2) & 15) == 0);
+    if (vec) {
+      for (int i = 2 * (blockIdx.x * blockDim.x + threadIdx.x); i < C.rows; i += 2 * gridDim.x * blockDim.x) {
+#pragma unroll 4
+        for (int j = 0; j < nc; ++j) {
+          double2 v = __ldg(reinterpret_cast<const double2*>(Pc.p + i + (size_t)j * Pc.ld));
+          v.x *= Pc.alpha;
+          v.y *= Pc.alpha;
+          *reinterpret_cast<double2*>(C.dst + i + (size_t)(col + j) * C.ldd) = v;
+          if (C.dst2) *reinterpret_cast<double2*>(C.dst2 + i + (size_t)(col + j) * C.ldd2) = v;
+        }
+      }
+    } else {
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < C.rows; i += gridDim.x * blockDim.x) {
+#pragma unroll 4
+        for (int j = 0; j < nc; ++j) {
+          const double v = Pc.alpha * Pc.p[i + (size_t)j * Pc.ld];
+          C.dst[i + (size_t)(col + j) * C.ldd] = v;
+          if (C.dst2) C.dst2[i + (size_t)(col + j) * C.ldd2] = v;
+        }
       }
     }
     col += nc;

@@ -228,6 +228,46 @@ def test_qr_and_applyq(dev, m, k, cl):
     assert np.abs(back(dX, m, c) - ref).max() <= 1e-12 * max(1, np.abs(ref).max())
 
 
+@pytest.mark.parametrize("rows,ld,off,two", [(256, 256, 0, True), (255, 256, 0, False), (300, 302, 1, True),
+                                             (64, 64, 2, False), (1, 2, 0, True)])
+def test_concat(dev, rows, ld, off, two):
+    """hq_concat: dst = [a1 P1 | a2 P2] (and the optional second copy), K into
+    the rank table; 16-byte path (even rows / leading dims, aligned bases) and
+    the element path (odd rows, odd offsets)."""
+    torch, lib = dev
+    rng = np.random.default_rng(rows + ld)
+    c1, c2 = 5, 3
+    P1 = rng.standard_normal((rows, c1)); P2 = rng.standard_normal((rows, c2))
+
+    def dev_cols(x):
+        buf = np.full(off + ld * x.shape[1] + 4, -3.0)
+        for j in range(x.shape[1]):
+            buf[off + j * ld: off + j * ld + rows] = x[:, j]
+        return torch.tensor(buf, device="cuda")
+    d1, d2 = dev_cols(P1), dev_cols(P2)
+    dst = torch.full((off + ld * (c1 + c2) + 4,), -3.0, dtype=torch.float64, device="cuda")
+    dst2 = torch.full((off + ld * (c1 + c2) + 4,), -3.0, dtype=torch.float64, device="cuda")
+    rank = torch.zeros(4, dtype=torch.int32, device="cuda")
+    rank[1] = c2
+    pieces = np.zeros(2, _abi.PIECE)
+    pieces[0] = (d1.data_ptr() + 8 * off, ld, c1, -1, 0, 0.5)
+    pieces[1] = (d2.data_ptr() + 8 * off, ld, 7, 1, 0, -2.0)   # capacity 7, run-time 3 columns
+    pr = np.zeros(1, _abi.CONCAT_PROB)
+    pr[0] = (dst.data_ptr() + 8 * off, dst2.data_ptr() + 8 * off if two else 0, ld, ld, rows, 0, 2, 2)
+    assert lib.hq_concat(None, put(torch, pr).data_ptr(), 1, put(torch, pieces).data_ptr(), rank.data_ptr(), rows) == 0
+    torch.cuda.synchronize()
+    assert int(rank[2].item()) == c1 + c2
+    ref = np.concatenate([0.5 * P1, -2.0 * P2], axis=1)
+    for d in ((dst, dst2) if two else (dst,)):
+        o = d.cpu().numpy()
+        got = np.stack([o[off + j * ld: off + j * ld + rows] for j in range(c1 + c2)], axis=1)
+        assert np.array_equal(got, ref)
+        o2 = o.copy()
+        for j in range(c1 + c2):
+            o2[off + j * ld: off + j * ld + rows] = -3.0
+        assert (o2 == -3.0).all()
+
+
 @pytest.mark.parametrize("trans,max_rows", [(0, None), (1, None), (0, 0), (1, 1024)])
 @pytest.mark.parametrize("m,k,c,ldx,off", [(64, 48, 40, 64, 0), (65, 33, 7, 66, 0), (65, 33, 7, 65, 0),
                                             (200, 150, 70, 202, 1), (200, 150, 70, 200, 2), (2, 2, 3, 2, 0),
