@@ -508,15 +508,16 @@ def main():
         top = max((k for k in per if acc.get(k, {}).get("flops", 0) > 0), key=lambda k: per[k][0])
         peak_fp64 = 37.16e12  # self-measured DMMA m8n8k4 FP64 (profiles/r01_fp64_peak.txt)
         ach = acc[top]["flops"] / (per[top][0] / 1e3)
-        traffic = None
+        traffic, traffic_all = None, {}
         try:   # DRAM bytes per launch of this kernel from the committed ncu --set full capture
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
-                traffic = json.load(fh).get(top, {}).get("dram_bytes_per_launch")
+            with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
+                traffic_all = json.load(fh)
+            traffic = traffic_all.get(top, {}).get("dram_bytes_per_launch")
         except (OSError, ValueError):
             pass
         line["roofline"] = {"kernel": top, "bound": "tensor", "achieved": ach / 1e12, "peak": peak_fp64 / 1e12,
                             "unit": "TFLOP/s", "frac": ach / peak_fp64, "traffic": traffic,
-                            "traffic_unit": "bytes/launch (dram__bytes_read+write, profiles/r01_traffic.json)",
+                            "traffic_unit": "bytes/launch (dram__bytes_read+write, profiles/r02_traffic.json)",
                             "peak_source": "self-measured FP64 DMMA peak (profiles/r01_fp64_peak.txt); "
                                            "MEASURED_PEAKS.json has no FP64 entry",
                             "flops_per_launch": acc[top]["flops"] / max(acc[top]["launches"], 1),
@@ -542,6 +543,8 @@ def main():
                 tf = a["flops"] / max(sec, 1e-12) / 1e12
                 rbk[k] = {"bound": "tensor", "achieved": tf, "peak": peak_fp64 / 1e12, "unit": "TFLOP/s",
                           "frac": tf / (peak_fp64 / 1e12), "flops_per_launch": a["flops"] / max(v[1], 1)}
+        for k in rbk:   # measured DRAM bytes of one captured launch of the class (ncu), where committed
+            rbk[k]["traffic"] = traffic_all.get(k, {}).get("dram_bytes_per_launch")
         line["roofline_by_kind"] = rbk
     if rank == 0 and not args.no_cpu_baseline and ws == 1:
         v_cpu, procs, cnt = cpu_throughput(args.config, n, rounds=1)
